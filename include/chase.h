@@ -1,0 +1,217 @@
+/*
+ * chase.h -- C-ABI of the B200-native ChASE hot path (arXiv 2309.15595):
+ * the 2D-distributed Chebyshev polynomial filter and the condition-driven CholeskyQR family.
+ *
+ * Citations: P:NNN = /root/reference/PAPER.md line, S:NNN = SPEC.md line; "Alg.k l.m" = line m
+ * of Algorithm k as printed.  Readings of silent/garbled passages are numbered #1..#24 in
+ * DESIGN.md ("Readings").
+ *
+ * Conventions shared by every entry point
+ *  - Matrices are column-major (BLAS convention).  Element type is double (CHASE_R64) or
+ *    interleaved complex double {re, im} (CHASE_C128, = cuDoubleComplex = torch.complex128).
+ *  - Device pointers are CUDA device memory owned by the caller (PyTorch allocates it).
+ *    Host pointers are read or written only during the call.
+ *  - All device work is enqueued on the handle's CUDA stream; calls return after enqueue
+ *    unless stated otherwise.
+ *  - The handle is not thread-safe; one handle per process/GPU.
+ *  - Collective calls (chase_filter, chase_cholqr) must be made by every rank of the grid with
+ *    identical scalar arguments (SPMD); otherwise the result is undefined or a hang.
+ *  - Argument errors are reported synchronously, before any device work, and leave all
+ *    buffers untouched.
+ */
+#ifndef CHASE_H_
+#define CHASE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CHASE_OK = 0,
+  CHASE_EINVAL = 1,   /* bad size / leading dimension / pointer / non-finite scalar          */
+  CHASE_EDEGREE = 2,  /* a degree odd, < 2, or degrees not non-decreasing      */
+  CHASE_EBOUNDS = 3,  /* e <= 0, or mu_1 inside the damped interval ((mu_1-c)/e > -1)         */
+  CHASE_ECHOL = 4,    /* Cholesky failed even on the shifted path; *info = pivot      */
+  CHASE_ECUDA = 5,    /* CUDA runtime / driver failure                                        */
+  CHASE_ENCCL = 6,    /* NCCL failure                                                         */
+  CHASE_ENOMEM = 7,   /* workspace missing or too small                                       */
+  CHASE_ESTATE = 8    /* call sequence error (e.g. no workspace set)                          */
+} chase_status_t;
+
+typedef enum { CHASE_R64 = 1, CHASE_C128 = 2 } chase_dtype_t;
+
+/* QR variants of Alg.4.  CHOL1 = CholeskyQR (cholDegree 1), CHOL2 = CholeskyQR2,
+ * SHIFTED = one shifted pass (POTRF(G + sI)) followed by CholeskyQR2 (reading #13). */
+typedef enum { CHASE_QR_CHOL1 = 1, CHASE_QR_CHOL2 = 2, CHASE_QR_SHIFTED = 3 } chase_qr_variant_t;
+
+/* Spectral bounds of Alg.1 l.2: mu_1 ~ lambda_min, mu_ne ~ lambda_{nev+nex},
+ * b_sup >= lambda_max.  The filter uses mu_1 for the scaling point (reading #2); c and e are
+ * passed separately and are authoritative. */
+typedef struct {
+  double mu_1, mu_ne, b_sup;
+} chase_bounds_t;
+
+/* Per-call statistics.  matvecs = sum_j d_j; steps = max degree D; qr_variant = the
+ * Alg.4 branch actually executed; qr_passes = Gram/POTRF/TRSM rounds executed. */
+typedef struct {
+  int64_t matvecs;
+  int32_t steps;
+  int32_t qr_variant;
+  int32_t qr_passes;
+  int32_t reserved;
+} chase_stats_t;
+
+/* Bookkeeping record of one filter step s (1-based in the paper, index s-1 here):
+ * k = #{j : d_j >= s} active columns, off = ncols - k first active column,
+ * comm = 0 for an odd step (H^H-side: result in B-layout, AllReduce over the column
+ * communicator) and 1 for an even step (result in C-layout, AllReduce over the row
+ * communicator), elems = complex/real elements in this rank's AllReduce message
+ * (n_c*k for odd, n_r*k for even); the AllReduce is skipped when that communicator has a
+ * single member (p == 1 for odd steps, q == 1 for even steps). */
+typedef struct {
+  int32_t k;
+  int32_t off;
+  int32_t comm;
+  int32_t reserved;
+  int64_t elems;
+} chase_step_record_t;
+
+typedef struct chase_handle_s* chase_handle_t;
+
+/* ---------------------------------------------------------------------------------------
+ * Setup (Alg.2 "Require": 2D grid with rcomm/ccomm; one GPU per rank).
+ * ------------------------------------------------------------------------------------- */
+
+/* Rank 0 calls this and distributes the 128 opaque bytes to every rank (the Python layer uses
+ * torch.distributed.broadcast).  Wraps ncclGetUniqueId.  Errors: CHASE_EINVAL (null id),
+ * CHASE_ENCCL. */
+chase_status_t chase_get_unique_id(uint8_t id[128]);
+
+/* Create a handle for rank (myrow, mycol) of a p x q grid holding block (myrow, mycol) of the
+ * N x N Hermitian/symmetric matrix under the block distribution of P:113 with the remainder
+ * rule of S:102 (the first N mod p grid rows get one extra row; same for columns).
+ * n_max = the largest number of vector columns later passed (nev+nex).
+ * id = the unique id from chase_get_unique_id (ignored, may be NULL, when p*q == 1).
+ * device = CUDA ordinal; cuda_stream = cudaStream_t to enqueue on (NULL = legacy default).
+ * World rank = myrow*q + mycol; the row communicator (rcomm) joins the q ranks of grid row
+ * myrow, the column communicator (ccomm) the p ranks of grid column mycol.
+ * Errors: CHASE_EINVAL (N < 1, n_max < 1 or > N, bad grid coordinates), CHASE_ECUDA,
+ * CHASE_ENCCL, CHASE_ENOMEM. */
+chase_status_t chase_create(chase_handle_t* h, chase_dtype_t dt, int64_t N, int64_t n_max, int p,
+                            int q, int myrow, int mycol, const uint8_t id[128], int device,
+                            void* cuda_stream);
+
+/* Change the stream later calls enqueue on. */
+chase_status_t chase_set_stream(chase_handle_t h, void* cuda_stream);
+
+/* Local block geometry of this rank: A_local is n_r x n_c, rows r0.., columns c0.. of A. */
+chase_status_t chase_local_dims(chase_handle_t h, int64_t* n_r, int64_t* n_c, int64_t* r0,
+                                int64_t* c0);
+
+/* Pure host function: the same geometry for any (N, p, q, i, j) without a handle. */
+chase_status_t chase_block_dims(int64_t N, int p, int q, int i, int j, int64_t* n_r,
+                                int64_t* n_c, int64_t* r0, int64_t* c0);
+
+/* Bytes of device workspace the handle needs: the B-layout block n_c x n_max, the
+ * n_max x n_max Gram matrix (Alg.3 l.3), and small scalars.  Memory model Eq.(2), P:216-223,
+ * minus the C2/B2/A buffers of the Rayleigh-Ritz step, which are out of scope. */
+chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes);
+
+/* Hand the handle `bytes` of caller-owned device memory (>= chase_workspace_size, 256-byte
+ * aligned).  The memory must stay valid until chase_destroy or the next set_workspace.
+ * Errors: CHASE_EINVAL (null / misaligned), CHASE_ENOMEM (too small). */
+chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes);
+
+/* ---------------------------------------------------------------------------------------
+ * Chebyshev filter -- Eq.(1), Alg.1 l.4, Alg.2 l.12, with the
+ * damped scalars of S:362 (reading #1):
+ *   sigma_1 = e/(mu_1 - c);  V_1 = (sigma_1/e)(A - cI)V_0;
+ *   sigma_s = 1/(2/sigma_1 - sigma_{s-1});
+ *   V_s = 2(sigma_s/e)(A - cI)V_{s-1} - sigma_{s-1} sigma_s V_{s-2}   (s = 2..D)
+ * Column j of V is replaced by V_{d_j}[:, j] = p_{d_j}(A) v_j with
+ * p_d(lambda) = T_d((lambda - c)/e) / T_d((mu_1 - c)/e).
+ * Odd steps compute A^H C into the B-layout workspace and all-reduce over ccomm; even steps
+ * compute A B back into V (C-layout) and all-reduce over rcomm, so no redistribution is
+ * needed and even degrees leave the result in V.  The -cI shift is applied by the
+ * rank whose block contains the diagonal rows (reading #6); the beta term is added by the
+ * first rank of the reducing communicator (reading #7).  A_local is never modified.
+ *
+ *  A_local  device, const: A[r0:r0+n_r, c0:c0+n_c], leading dimension lda >= n_r.
+ *  V        device, in/out: rows [r0, r0+n_r) of the N x ncols block (C-layout), ldv >= n_r.
+ *           Must be identical on all q ranks of a grid row on input; it is identical
+ *           on output.  lda and ldv times the element size must be multiples of 16 bytes
+ *           (TMA row pitch; i.e. even for CHASE_R64), pointers 16-byte aligned.
+ *  ncols    1..n_max (Alg.2 filters C[:, locked+1:]).
+ *  degrees  host, ncols int32: even, >= 2, non-decreasing (sorted, Alg.1 l.12 P:103).
+ *  c, e     centre and half-width of the damped interval [mu_ne, b_sup] (Alg.2 l.3).
+ *  bounds   host: mu_1 sets the scaling point; mu_ne, b_sup informational (reading #2).
+ *  stats    host, nullable: matvecs and steps.
+ * Errors: CHASE_EINVAL, CHASE_EDEGREE, CHASE_EBOUNDS, CHASE_ESTATE (no workspace),
+ * CHASE_ECUDA, CHASE_ENCCL.  Returns after enqueue. */
+chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, void* V,
+                            int64_t ldv, int64_t ncols, const int32_t* degrees, double c,
+                            double e, const chase_bounds_t* bounds, chase_stats_t* stats);
+
+/* The per-step record of the last chase_filter call on this handle (the schedule that was
+ * actually launched).  rec: host array of max_steps entries; *nsteps = D. */
+chase_status_t chase_filter_record(chase_handle_t h, int32_t max_steps, chase_step_record_t* rec,
+                                   int32_t* nsteps, int64_t* matvecs);
+
+/* Pure host function: the schedule chase_filter would run for rank (myrow, mycol). */
+chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int mycol, int64_t ncols,
+                                     const int32_t* degrees, int32_t max_steps,
+                                     chase_step_record_t* rec, int32_t* nsteps,
+                                     int64_t* matvecs);
+
+/* ---------------------------------------------------------------------------------------
+ * 1D-CAQR -- Alg.4 over the column communicator, Alg.2 l.14.
+ * Variant: cond_est > 1e8 -> shifted CholeskyQR2; cond_est < 20 -> CholeskyQR; else
+ * CholeskyQR2 (ties -> CholeskyQR2, reading #9).  Each pass (Alg.3): G = V^H V (local Gram,
+ * then AllReduce SUM over ccomm), [shifted pass: norm = ||V||_F^2 = Re tr(G) (reading #12),
+ * s = 11(N*ncols + ncols(ncols+1)) u norm, u = 2^-53, G += sI], G = R^H R (POTRF, R upper
+ * with positive real diagonal), V = V R^{-1} (TRSM).  If the first POTRF of CholeskyQR or
+ * CholeskyQR2 fails (V untouched) the call escalates to the shifted path (reading #14).
+ *
+ *  V        device, in/out: the C-layout block as for chase_filter, ldv >= n_r (16-byte
+ *           pitch as for chase_filter).
+ *  ncols    1..n_max columns to orthonormalise (all given columns; reading #16).
+ *  cond_est >= 1, e.g. from chase_cond_est (Alg.5).
+ *  stats    host, nullable: qr_variant (executed branch) and qr_passes.
+ *  info     host, nullable: 0, or the 1-based failing pivot of the last POTRF.
+ * Synchronises the stream once per POTRF (4-byte info read).
+ * Errors: CHASE_EINVAL (bad sizes, cond_est < 1 or NaN), CHASE_ECHOL (shifted POTRF failed;
+ * the caller decides on Householder QR, P:299 -- out of scope here), CHASE_ESTATE,
+ * CHASE_ECUDA, CHASE_ENCCL. */
+chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols, double cond_est,
+                            chase_stats_t* stats, int32_t* info);
+
+/* Alg.5, host, pure: t' = (ritz[0]-c)/e, t = (ritz[locked]-c)/e,
+ * |rho| = max(|t - sqrt(t^2-1)|, |t + sqrt(t^2-1)|) (complex sqrt: 1 when |t| <= 1),
+ * d = degrees[locked], d_M = max(degrees[locked..n-1]); returns |rho|^d |rho'|^(d_M - d).
+ * ritz: host array of n Ritz values (ascending); degrees: host, n entries.
+ * Returns NaN on invalid input (n < 1, locked outside [0, n), e <= 0). */
+double chase_cond_est(const double* ritz, int64_t n, double c, double e, const int32_t* degrees,
+                      int64_t locked);
+
+/* Alg.4 l.6, host, pure: s = 11 (m n + n (n + 1)) u norm, u = 2^-53. */
+double chase_shift_value(int64_t m, int64_t n, double norm);
+
+/* ---------------------------------------------------------------------------------------
+ * Measurement support (bench.py): when enabled, CUDA events bracket every launch on the
+ * handle's stream; chase_profile_read synchronises, returns per-category device time (ms)
+ * and launch counts since the last read, and resets.  Categories:
+ *   0 HEMM (filter steps)  1 AllReduce  2 Gram  3 POTRF  4 TRSM  5 other kernels
+ * ms and launches are host arrays of 6 entries. */
+chase_status_t chase_profile_enable(chase_handle_t h, int enable);
+chase_status_t chase_profile_read(chase_handle_t h, double ms[6], int64_t launches[6]);
+
+chase_status_t chase_destroy(chase_handle_t h);
+const char* chase_status_string(chase_status_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHASE_H_ */

@@ -1,0 +1,825 @@
+// chase.cu -- host side of libchase.so: handle, argument validation, the filter step driver,
+// the 1D-CAQR driver (Alg.4) and the C-ABI declared in include/chase.h.
+//
+// Every step of the hot path runs in this library's kernels (zgemm.cuh, qr_kernels.cuh) and
+// NCCL collectives on the handle's stream; there is no CPU fallback.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "chase.h"
+#include "dgemm.cuh"
+#include "qr_kernels.cuh"
+#include "zgemm.cuh"
+
+using namespace chase;
+
+// ==================================================================== utilities
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t err__ = (x);                                                          \
+    if (err__ != cudaSuccess) {                                                       \
+      fprintf(stderr, "[chase] CUDA error %s at %s:%d\n", cudaGetErrorString(err__), \
+              __FILE__, __LINE__);                                                    \
+      return CHASE_ECUDA;                                                             \
+    }                                                                                 \
+  } while (0)
+#define NCCL_TRY(x)                                                                   \
+  do {                                                                                \
+    ncclResult_t r__ = (x);                                                           \
+    if (r__ != ncclSuccess) {                                                         \
+      fprintf(stderr, "[chase] NCCL error %s at %s:%d\n", ncclGetErrorString(r__),    \
+              __FILE__, __LINE__);                                                    \
+      return CHASE_ENCCL;                                                             \
+    }                                                                                 \
+  } while (0)
+#define STATUS_TRY(x)                 \
+  do {                                \
+    chase_status_t st__ = (x);        \
+    if (st__ != CHASE_OK) return st__; \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D FP64 tensor map over a column-major matrix of `rows` x `cols` elements of `esize` bytes
+// (16 = complex, 8 = real), leading dimension ld (elements), box = box_rows x box_cols elements,
+// 128-byte swizzle (box_rows * esize must be 128).
+static chase_status_t make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
+                               int64_t ld, int esize, int box_rows, int box_cols) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return CHASE_ECUDA;
+  const int per = esize / 8;
+  cuuint64_t dims[2] = {(cuuint64_t)(rows * per), (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esize)};
+  cuuint32_t box[2] = {(cuuint32_t)(box_rows * per), (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "[chase] cuTensorMapEncodeTiled failed (%d): rows %lld cols %lld ld %lld\n",
+            (int)r, (long long)rows, (long long)cols, (long long)ld);
+    return CHASE_ECUDA;
+  }
+  return CHASE_OK;
+}
+
+static void block_part(int64_t N, int P, int k, int64_t* size, int64_t* start) {
+  const int64_t b = N / P, rem = N % P;
+  *size = b + (k < rem ? 1 : 0);
+  *start = k * b + (k < rem ? k : rem);
+}
+
+// ==================================================================== handle
+enum { CAT_HEMM = 0, CAT_ALLREDUCE, CAT_GRAM, CAT_POTRF, CAT_TRSM, CAT_OTHER, CAT_N };
+
+struct chase_handle_s {
+  chase_dtype_t dt;
+  int64_t N, n_max;
+  int p, q, myrow, mycol;
+  int64_t n_r, n_c, r0, c0;
+  int device;
+  cudaStream_t stream;
+  ncclComm_t world = nullptr, rcomm = nullptr, ccomm = nullptr;
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* Bws = nullptr;      // n_c x n_max (B-layout block)
+  void* Gws = nullptr;      // n_max x n_max (Gram / R)
+  int* d_info = nullptr;
+  double* d_shift = nullptr;
+  int* h_info = nullptr;    // pinned
+  // bookkeeping of the last filter call
+  std::vector<chase_step_record_t> record;
+  int64_t last_matvecs = 0;
+  // profiling
+  bool profiling = false;
+  struct Ev {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  std::vector<Ev> evs;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches[CAT_N] = {0};
+
+  cudaEvent_t ev_get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+struct ProfScope {
+  chase_handle_s* h;
+  int cat;
+  cudaEvent_t a = nullptr;
+  ProfScope(chase_handle_s* h_, int c, int nlaunch) : h(h_), cat(c) {
+    h->launches[c] += nlaunch;
+    if (h->profiling) {
+      a = h->ev_get();
+      cudaEventRecord(a, h->stream);
+    }
+  }
+  ~ProfScope() {
+    if (h->profiling) {
+      cudaEvent_t b = h->ev_get();
+      cudaEventRecord(b, h->stream);
+      h->evs.push_back({cat, a, b});
+    }
+  }
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+// Leading dimension of library-owned buffers: even, so every column starts 16-byte aligned
+// (TMA requires 16-byte global strides; matters for real double).
+static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
+
+static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
+
+static void ws_layout(const chase_handle_s* h, size_t* b_off, size_t* g_off, size_t* info_off,
+                      size_t* s_off, size_t* total) {
+  const size_t es = esize_of(h->dt);
+  size_t off = 0;
+  *b_off = off;
+  off += align256((size_t)pad_ld(h->n_c) * h->n_max * es);
+  *g_off = off;
+  off += align256((size_t)pad_ld(h->n_max) * h->n_max * es);
+  *info_off = off;
+  off += 256;
+  *s_off = off;
+  off += 256;
+  *total = off;
+}
+
+// ==================================================================== GEMM launchers
+static bool g_attr_done[2][2] = {{false, false}, {false, false}};
+
+static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
+                                   const CUtensorMap& tX, const ZGemmArgs& a) {
+  if (a.M <= 0 || a.N <= 0) return CHASE_OK;
+  dim3 grid((a.N + ZG_BN - 1) / ZG_BN, (a.M + ZG_BM - 1) / ZG_BM);
+  if (conj) {
+    if (!g_attr_done[1][0]) {
+      CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ZG_SMEM_BYTES));
+      g_attr_done[1][0] = true;
+    }
+    zgemm_kernel<true><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  } else {
+    if (!g_attr_done[0][0]) {
+      CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
+      g_attr_done[0][0] = true;
+    }
+    zgemm_kernel<false><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CHASE_OK;
+}
+
+static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
+                                   const CUtensorMap& tX, const DGemmArgs& a) {
+  if (a.M <= 0 || a.N <= 0) return CHASE_OK;
+  dim3 grid((a.N + DG_BN - 1) / DG_BN, (a.M + DG_BM - 1) / DG_BM);
+  if (trans) {
+    if (!g_attr_done[1][1]) {
+      CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    DG_SMEM_BYTES));
+      g_attr_done[1][1] = true;
+    }
+    dgemm_kernel<true><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  } else {
+    if (!g_attr_done[0][1]) {
+      CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
+      g_attr_done[0][1] = true;
+    }
+    dgemm_kernel<false><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CHASE_OK;
+}
+
+// One generic GEMM request, dispatched on the handle's dtype.  Pointers are element pointers
+// of the handle's dtype; offsets are in elements.
+struct GemmReq {
+  bool conj;                 // opA = A^H (A^T for real)
+  const CUtensorMap* tA;
+  const CUtensorMap* tX;
+  int M, N, K, a_d0, a_d1, x_k0, x_n0;
+  void* out;
+  int64_t ldo;
+  const void* xin;
+  int64_t ldx;
+  double alpha, beta, c;
+  int use_beta, band_lo, band_hi, band_shift, upper_only;
+  const int* abort_flag;
+};
+
+static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
+  if (h->dt == CHASE_C128) {
+    ZGemmArgs a;
+    a.M = r.M; a.N = r.N; a.K = r.K;
+    a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
+    a.out = static_cast<double2*>(r.out); a.ldo = r.ldo;
+    a.xin = static_cast<const double2*>(r.xin); a.ldx = r.ldx;
+    a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
+    a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
+    a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
+  }
+  DGemmArgs a;
+  a.M = r.M; a.N = r.N; a.K = r.K;
+  a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
+  a.out = static_cast<double*>(r.out); a.ldo = r.ldo;
+  a.xin = static_cast<const double*>(r.xin); a.ldx = r.ldx;
+  a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
+  a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
+  a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
+}
+
+// Tensor maps for the three roles a matrix plays in the GEMM (box shapes of zgemm / dgemm).
+enum MapRole { ROLE_A_NOTRANS, ROLE_A_TRANS, ROLE_X };
+static chase_status_t make_role_map(const chase_handle_s* h, CUtensorMap* m, const void* base,
+                                    int64_t rows, int64_t cols, int64_t ld, MapRole role) {
+  if (h->dt == CHASE_C128) {
+    const int bc = role == ROLE_A_NOTRANS ? 8 : role == ROLE_A_TRANS ? ZG_BM : ZG_BN;
+    return make_map(m, base, rows, cols, ld, 16, 8, bc);
+  }
+  const int bc = role == ROLE_A_NOTRANS ? DG_BK : role == ROLE_A_TRANS ? DG_BM : DG_BN;
+  return make_map(m, base, rows, cols, ld, 8, 16, bc);
+}
+
+static chase_status_t allreduce(chase_handle_s* h, void* buf, size_t elems, ncclComm_t comm) {
+  ProfScope ps(h, CAT_ALLREDUCE, 0);
+  const size_t nd = elems * (h->dt == CHASE_C128 ? 2 : 1);
+  NCCL_TRY(ncclAllReduce(buf, buf, nd, ncclDouble, ncclSum, comm, h->stream));
+  return CHASE_OK;
+}
+
+// Column-by-column AllReduce of a strided block (rows n_r of each column), one NCCL group.
+static chase_status_t allreduce_cols(chase_handle_s* h, void* buf, int64_t rows, int64_t ld,
+                                     int64_t cols, ncclComm_t comm) {
+  ProfScope ps(h, CAT_ALLREDUCE, 0);
+  const size_t es = esize_of(h->dt), per = es / 8;
+  NCCL_TRY(ncclGroupStart());
+  for (int64_t j = 0; j < cols; ++j) {
+    char* p = static_cast<char*>(buf) + (size_t)j * ld * es;
+    NCCL_TRY(ncclAllReduce(p, p, (size_t)rows * per, ncclDouble, ncclSum, comm, h->stream));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return CHASE_OK;
+}
+
+// ==================================================================== schedule (pure)
+static chase_status_t validate_degrees(int64_t ncols, const int32_t* degrees) {
+  if (!degrees) return CHASE_EINVAL;
+  for (int64_t j = 0; j < ncols; ++j) {
+    const int32_t d = degrees[j];
+    if (d < 2 || (d % 2) != 0) return CHASE_EDEGREE;
+    if (j > 0 && d < degrees[j - 1]) return CHASE_EDEGREE;
+  }
+  return CHASE_OK;
+}
+
+static void build_schedule(int64_t n_r, int64_t n_c, int64_t ncols, const int32_t* degrees,
+                           std::vector<chase_step_record_t>* rec, int64_t* matvecs) {
+  const int32_t D = degrees[ncols - 1];
+  rec->assign(D, chase_step_record_t{});
+  int64_t mv = 0;
+  for (int64_t j = 0; j < ncols; ++j) mv += degrees[j];
+  int64_t first = 0;  // first column with d_j >= s (degrees sorted)
+  for (int32_t s = 1; s <= D; ++s) {
+    while (first < ncols && degrees[first] < s) ++first;
+    chase_step_record_t& r = (*rec)[s - 1];
+    r.k = (int32_t)(ncols - first);
+    r.off = (int32_t)first;
+    r.comm = (s % 2 == 1) ? 0 : 1;
+    r.reserved = 0;
+    r.elems = (int64_t)r.k * (s % 2 == 1 ? n_c : n_r);
+  }
+  *matvecs = mv;
+}
+
+// ==================================================================== C-ABI
+extern "C" {
+
+const char* chase_status_string(chase_status_t s) {
+  switch (s) {
+    case CHASE_OK: return "CHASE_OK";
+    case CHASE_EINVAL: return "CHASE_EINVAL: invalid argument";
+    case CHASE_EDEGREE: return "CHASE_EDEGREE: degrees must be even, >= 2 and non-decreasing";
+    case CHASE_EBOUNDS: return "CHASE_EBOUNDS: e <= 0 or mu_1 inside the damped interval";
+    case CHASE_ECHOL: return "CHASE_ECHOL: Cholesky factorisation failed";
+    case CHASE_ECUDA: return "CHASE_ECUDA: CUDA failure";
+    case CHASE_ENCCL: return "CHASE_ENCCL: NCCL failure";
+    case CHASE_ENOMEM: return "CHASE_ENOMEM: workspace missing or too small";
+    case CHASE_ESTATE: return "CHASE_ESTATE: invalid call sequence";
+  }
+  return "CHASE_?: unknown status";
+}
+
+chase_status_t chase_get_unique_id(uint8_t id[128]) {
+  if (!id) return CHASE_EINVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId uid;
+  NCCL_TRY(ncclGetUniqueId(&uid));
+  memcpy(id, &uid, 128);
+  return CHASE_OK;
+}
+
+chase_status_t chase_block_dims(int64_t N, int p, int q, int i, int j, int64_t* n_r,
+                                int64_t* n_c, int64_t* r0, int64_t* c0) {
+  if (N < 1 || p < 1 || q < 1 || i < 0 || i >= p || j < 0 || j >= q || !n_r || !n_c || !r0 ||
+      !c0 || p > N || q > N)
+    return CHASE_EINVAL;
+  block_part(N, p, i, n_r, r0);
+  block_part(N, q, j, n_c, c0);
+  return CHASE_OK;
+}
+
+chase_status_t chase_create(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
+                            int p, int q, int myrow, int mycol, const uint8_t id[128], int device,
+                            void* cuda_stream) {
+  if (!out) return CHASE_EINVAL;
+  *out = nullptr;
+  if (dt != CHASE_R64 && dt != CHASE_C128) return CHASE_EINVAL;
+  if (N < 1 || n_max < 1 || n_max > N || N > (int64_t)INT32_MAX) return CHASE_EINVAL;
+  if (p < 1 || q < 1 || myrow < 0 || myrow >= p || mycol < 0 || mycol >= q) return CHASE_EINVAL;
+  if (p > N || q > N) return CHASE_EINVAL;
+  if (p * q > 1 && !id) return CHASE_EINVAL;
+  chase_handle_s* h = new chase_handle_s();
+  h->dt = dt;
+  h->N = N;
+  h->n_max = n_max;
+  h->p = p;
+  h->q = q;
+  h->myrow = myrow;
+  h->mycol = mycol;
+  block_part(N, p, myrow, &h->n_r, &h->r0);
+  block_part(N, q, mycol, &h->n_c, &h->c0);
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&h->h_info, sizeof(int)) != cudaSuccess) {
+    delete h;
+    return CHASE_ECUDA;
+  }
+  if (p * q > 1) {
+    ncclUniqueId uid;
+    memcpy(&uid, id, 128);
+    const int rank = myrow * q + mycol;
+    ncclResult_t r = ncclCommInitRank(&h->world, p * q, uid, rank);
+    if (r == ncclSuccess) r = ncclCommSplit(h->world, myrow, mycol, &h->rcomm, nullptr);
+    if (r == ncclSuccess) r = ncclCommSplit(h->world, mycol, myrow, &h->ccomm, nullptr);
+    if (r != ncclSuccess) {
+      fprintf(stderr, "[chase] NCCL setup failed: %s\n", ncclGetErrorString(r));
+      chase_destroy(h);
+      return CHASE_ENCCL;
+    }
+  }
+  *out = h;
+  return CHASE_OK;
+}
+
+chase_status_t chase_set_stream(chase_handle_t h, void* cuda_stream) {
+  if (!h) return CHASE_EINVAL;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  return CHASE_OK;
+}
+
+chase_status_t chase_local_dims(chase_handle_t h, int64_t* n_r, int64_t* n_c, int64_t* r0,
+                                int64_t* c0) {
+  if (!h || !n_r || !n_c || !r0 || !c0) return CHASE_EINVAL;
+  *n_r = h->n_r;
+  *n_c = h->n_c;
+  *r0 = h->r0;
+  *c0 = h->c0;
+  return CHASE_OK;
+}
+
+chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes) {
+  if (!h || !bytes) return CHASE_EINVAL;
+  size_t b, g, i, s, t;
+  ws_layout(h, &b, &g, &i, &s, &t);
+  *bytes = t;
+  return CHASE_OK;
+}
+
+chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
+  if (!h || !dptr || (reinterpret_cast<uintptr_t>(dptr) & 255) != 0) return CHASE_EINVAL;
+  size_t b, g, i, s, t;
+  ws_layout(h, &b, &g, &i, &s, &t);
+  if (bytes < t) return CHASE_ENOMEM;
+  char* base = static_cast<char*>(dptr);
+  h->ws = dptr;
+  h->ws_bytes = bytes;
+  h->Bws = base + b;
+  h->Gws = base + g;
+  h->d_info = reinterpret_cast<int*>(base + i);
+  h->d_shift = reinterpret_cast<double*>(base + s);
+  return CHASE_OK;
+}
+
+chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int mycol, int64_t ncols,
+                                     const int32_t* degrees, int32_t max_steps,
+                                     chase_step_record_t* rec, int32_t* nsteps,
+                                     int64_t* matvecs) {
+  int64_t n_r, n_c, r0, c0;
+  STATUS_TRY(chase_block_dims(N, p, q, myrow, mycol, &n_r, &n_c, &r0, &c0));
+  if (ncols < 1 || ncols > N || !nsteps) return CHASE_EINVAL;
+  STATUS_TRY(validate_degrees(ncols, degrees));
+  std::vector<chase_step_record_t> r;
+  int64_t mv;
+  build_schedule(n_r, n_c, ncols, degrees, &r, &mv);
+  *nsteps = (int32_t)r.size();
+  if (matvecs) *matvecs = mv;
+  if (rec) {
+    if (max_steps < (int32_t)r.size()) return CHASE_EINVAL;
+    memcpy(rec, r.data(), r.size() * sizeof(chase_step_record_t));
+  }
+  return CHASE_OK;
+}
+
+chase_status_t chase_filter_record(chase_handle_t h, int32_t max_steps, chase_step_record_t* rec,
+                                   int32_t* nsteps, int64_t* matvecs) {
+  if (!h || !nsteps) return CHASE_EINVAL;
+  *nsteps = (int32_t)h->record.size();
+  if (matvecs) *matvecs = h->last_matvecs;
+  if (rec) {
+    if (max_steps < (int32_t)h->record.size()) return CHASE_EINVAL;
+    memcpy(rec, h->record.data(), h->record.size() * sizeof(chase_step_record_t));
+  }
+  return CHASE_OK;
+}
+
+// Eq.(1) with the S:362 scalars; odd steps H^H-side into B, even steps into C.
+chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, void* V,
+                            int64_t ldv, int64_t ncols, const int32_t* degrees, double c,
+                            double e, const chase_bounds_t* bounds, chase_stats_t* stats) {
+  if (!h || !A_local || !V || !bounds) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max) return CHASE_EINVAL;
+  if (lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
+  if (!std::isfinite(c) || !std::isfinite(e) || !std::isfinite(bounds->mu_1)) return CHASE_EINVAL;
+  STATUS_TRY(validate_degrees(ncols, degrees));
+  if (!(e > 0.0)) return CHASE_EBOUNDS;
+  const double t1 = (bounds->mu_1 - c) / e;
+  if (!(t1 <= -1.0)) return CHASE_EBOUNDS;
+  if (!h->ws) return CHASE_ESTATE;
+  const size_t es = esize_of(h->dt);
+  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
+    return CHASE_EINVAL;
+  if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;   // TMA pitch
+
+  std::vector<chase_step_record_t> rec;
+  int64_t mv;
+  build_schedule(h->n_r, h->n_c, ncols, degrees, &rec, &mv);
+  const int D = (int)rec.size();
+
+  // recurrence scalars: alpha_1 = sigma_1/e, beta_1 = 0; alpha_s = 2 sigma_s/e,
+  // beta_s = -sigma_{s-1} sigma_s
+  std::vector<double> alpha(D), beta(D);
+  const double sigma_1 = e / (bounds->mu_1 - c);
+  double sigma = sigma_1;
+  alpha[0] = sigma_1 / e;
+  beta[0] = 0.0;
+  for (int s = 2; s <= D; ++s) {
+    const double sigma_prev = sigma;
+    sigma = 1.0 / (2.0 / sigma_1 - sigma_prev);
+    alpha[s - 1] = 2.0 * sigma / e;
+    beta[s - 1] = -sigma_prev * sigma;
+  }
+
+  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
+  CUtensorMap tA_nt, tA_t, tC, tB;
+  STATUS_TRY(make_role_map(h, &tA_nt, A_local, n_r, n_c, lda, ROLE_A_NOTRANS));
+  STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &tC, V, n_r, ncols, ldv, ROLE_X));
+  STATUS_TRY(make_role_map(h, &tB, h->Bws, n_c, ncols, ldb, ROLE_X));
+  char* Vc = static_cast<char*>(V);
+  char* Bc = static_cast<char*>(h->Bws);
+
+  for (int s = 1; s <= D; ++s) {
+    const chase_step_record_t& r = rec[s - 1];
+    GemmReq g;
+    g.alpha = alpha[s - 1];
+    g.beta = beta[s - 1];
+    g.c = c;
+    g.upper_only = 0;
+    g.abort_flag = nullptr;
+    g.x_k0 = 0;
+    g.x_n0 = r.off;
+    g.a_d0 = 0;
+    g.a_d1 = 0;
+    g.N = r.k;
+    if (s % 2 == 1) {
+      // B_j = alpha (A_ij^H C_i - c band(C_i)) + [i == 0, s > 1] beta B_j
+      g.conj = true;
+      g.tA = &tA_t;
+      g.tX = &tC;
+      g.M = (int)n_c;
+      g.K = (int)n_r;
+      g.out = Bc + (size_t)r.off * ldb * es;
+      g.ldo = ldb;
+      g.xin = Vc + (size_t)r.off * ldv * es;
+      g.ldx = ldv;
+      g.band_lo = (int)std::max<int64_t>(0, h->r0 - h->c0);
+      g.band_hi = (int)std::min<int64_t>(n_c, h->r0 + n_r - h->c0);
+      g.band_shift = (int)(h->c0 - h->r0);
+      g.use_beta = (h->myrow == 0 && s > 1) ? 1 : 0;
+    } else {
+      // C_i = alpha (A_ij B_j - c band(B_j)) + [j == 0] beta C_i
+      g.conj = false;
+      g.tA = &tA_nt;
+      g.tX = &tB;
+      g.M = (int)n_r;
+      g.K = (int)n_c;
+      g.out = Vc + (size_t)r.off * ldv * es;
+      g.ldo = ldv;
+      g.xin = Bc + (size_t)r.off * ldb * es;
+      g.ldx = ldb;
+      g.band_lo = (int)std::max<int64_t>(0, h->c0 - h->r0);
+      g.band_hi = (int)std::min<int64_t>(n_r, h->c0 + n_c - h->r0);
+      g.band_shift = (int)(h->r0 - h->c0);
+      g.use_beta = (h->mycol == 0) ? 1 : 0;
+    }
+    {
+      ProfScope ps(h, CAT_HEMM, 1);
+      STATUS_TRY(run_gemm(h, g));
+    }
+    if (s % 2 == 1 && h->p > 1) STATUS_TRY(allreduce(h, g.out, (size_t)ldb * r.k, h->ccomm));
+    if (s % 2 == 0 && h->q > 1) {
+      if (ldv == n_r)
+        STATUS_TRY(allreduce(h, g.out, (size_t)n_r * r.k, h->rcomm));
+      else
+        STATUS_TRY(allreduce_cols(h, g.out, n_r, ldv, r.k, h->rcomm));
+    }
+  }
+  h->record = rec;
+  h->last_matvecs = mv;
+  if (stats) {
+    stats->matvecs = mv;
+    stats->steps = D;
+  }
+  return CHASE_OK;
+}
+
+}  // extern "C"
+
+// ==================================================================== CholeskyQR (Alg.3/4)
+namespace {
+
+template <typename T>
+void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n, int rest) {
+  potrf_diag_kernel<T><<<1, 256, 0, h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info);
+  h->launches[CAT_POTRF]++;
+  if (rest > 0) {
+    potrf_panel_kernel<T><<<(rest + PANEL_THREADS - 1) / PANEL_THREADS, PANEL_THREADS,
+                            panel_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, n,
+                                                          h->d_info);
+    h->launches[CAT_POTRF]++;
+  }
+}
+
+struct QrMaps {
+  CUtensorMap vA_t, vA_nt, vX, gA_t, gX;
+};
+
+// One Gram/POTRF/TRSM round; returns CHASE_ECHOL with *info set when POTRF fails (V untouched).
+chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool shifted,
+                           const QrMaps& mp, int* info) {
+  const size_t es = esize_of(h->dt);
+  const int64_t n_r = h->n_r;
+  char* G = static_cast<char*>(h->Gws);
+  char* Vc = static_cast<char*>(V);
+  const int64_t ldg = pad_ld(n);
+  // Gram G = V^H V (upper tiles), Alg.3 l.3
+  {
+    GemmReq g{};
+    g.conj = true; g.tA = &mp.vA_t; g.tX = &mp.vX;
+    g.M = n; g.N = n; g.K = (int)n_r;
+    g.out = G; g.ldo = ldg; g.xin = nullptr; g.ldx = 0;
+    g.alpha = 1.0; g.beta = 0.0; g.c = 0.0; g.use_beta = 0;
+    g.band_lo = g.band_hi = 0; g.band_shift = 0; g.upper_only = 1; g.abort_flag = nullptr;
+    ProfScope ps(h, CAT_GRAM, 1);
+    STATUS_TRY(run_gemm(h, g));
+  }
+  // Alg.3 l.4 AllReduce over the column communicator
+  if (h->p > 1) STATUS_TRY(allreduce(h, G, (size_t)ldg * n, h->ccomm));
+  if (shifted) {
+    ProfScope ps(h, CAT_OTHER, 1);
+    if (h->dt == CHASE_C128)
+      shift_kernel<double2><<<1, 256, 0, h->stream>>>(reinterpret_cast<double2*>(G), ldg, n, h->N, h->d_shift);
+    else
+      shift_kernel<double><<<1, 256, 0, h->stream>>>(reinterpret_cast<double*>(G), ldg, n, h->N, h->d_shift);
+    CUDA_TRY(cudaGetLastError());
+  }
+  // POTRF, blocked right-looking, Alg.3 l.5
+  {
+    ProfScope ps(h, CAT_POTRF, 0);
+    CUDA_TRY(cudaMemsetAsync(h->d_info, 0, sizeof(int), h->stream));
+    for (int kb = 0; kb < n; kb += QR_NB) {
+      const int nb = std::min(QR_NB, n - kb);
+      const int rest = n - kb - nb;
+      if (h->dt == CHASE_C128)
+        potrf_blocks<double2>(h, G, ldg, kb, nb, n, rest);
+      else
+        potrf_blocks<double>(h, G, ldg, kb, nb, n, rest);
+      CUDA_TRY(cudaGetLastError());
+      if (rest > 0) {
+        // trailing HERK: G[j, l] -= sum_a conj(R[a, j]) R[a, l], a in the panel, j <= l
+        GemmReq g{};
+        g.conj = true; g.tA = &mp.gA_t; g.tX = &mp.gX;
+        g.M = rest; g.N = rest; g.K = nb;
+        g.a_d0 = kb; g.a_d1 = kb + nb; g.x_k0 = kb; g.x_n0 = kb + nb;
+        g.out = G + ((size_t)(kb + nb) + (size_t)(kb + nb) * ldg) * es; g.ldo = ldg;
+        g.alpha = -1.0; g.beta = 1.0; g.c = 0.0; g.use_beta = 1;
+        g.band_lo = g.band_hi = 0; g.upper_only = 1; g.abort_flag = h->d_info;
+        STATUS_TRY(run_gemm(h, g));
+        h->launches[CAT_POTRF]++;
+      }
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->h_info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  *info = *h->h_info;
+  if (*info != 0) return CHASE_ECHOL;
+  // TRSM V <- V R^{-1}, right-looking blocked, Alg.3 l.6
+  {
+    ProfScope ps(h, CAT_TRSM, 0);
+    for (int kb = 0; kb < n; kb += QR_NB) {
+      const int nb = std::min(QR_NB, n - kb);
+      const int rest = n - kb - nb;
+      const int grid = (int)((n_r + TRSM_THREADS - 1) / TRSM_THREADS);
+      if (h->dt == CHASE_C128)
+        trsm_diag_kernel<double2><<<grid, TRSM_THREADS, trsm_smem<double2>(), h->stream>>>(
+            reinterpret_cast<double2*>(V), ldv, (int)n_r, reinterpret_cast<const double2*>(G), ldg, kb, nb);
+      else
+        trsm_diag_kernel<double><<<grid, TRSM_THREADS, trsm_smem<double>(), h->stream>>>(
+            reinterpret_cast<double*>(V), ldv, (int)n_r, reinterpret_cast<const double*>(G), ldg, kb, nb);
+      CUDA_TRY(cudaGetLastError());
+      h->launches[CAT_TRSM]++;
+      if (rest > 0) {
+        // V[:, kb+nb:] -= V[:, kb:kb+nb] R[kb:kb+nb, kb+nb:]
+        GemmReq g{};
+        g.conj = false; g.tA = &mp.vA_nt; g.tX = &mp.gX;
+        g.M = (int)n_r; g.N = rest; g.K = nb;
+        g.a_d0 = 0; g.a_d1 = kb; g.x_k0 = kb; g.x_n0 = kb + nb;
+        g.out = Vc + (size_t)(kb + nb) * ldv * es; g.ldo = ldv;
+        g.alpha = -1.0; g.beta = 1.0; g.c = 0.0; g.use_beta = 1;
+        g.band_lo = g.band_hi = 0; g.upper_only = 0; g.abort_flag = nullptr;
+        STATUS_TRY(run_gemm(h, g));
+        h->launches[CAT_TRSM]++;
+      }
+    }
+  }
+  return CHASE_OK;
+}
+
+bool g_qr_attr_done = false;
+
+}  // namespace
+
+extern "C" {
+
+chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols,
+                            double cond_est, chase_stats_t* stats, int32_t* info_out) {
+  if (!h || !V) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
+  if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;   // TMA pitch
+  if (!(cond_est >= 1.0)) return CHASE_EINVAL;   // also rejects NaN
+  if (!h->ws) return CHASE_ESTATE;
+  if (reinterpret_cast<uintptr_t>(V) & 15) return CHASE_EINVAL;
+  if (!g_qr_attr_done) {
+    CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double2>()));
+    CUDA_TRY(cudaFuncSetAttribute(trsm_diag_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem<double2>()));
+    CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double>()));
+    CUDA_TRY(cudaFuncSetAttribute(trsm_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, trsm_smem<double>()));
+    g_qr_attr_done = true;
+  }
+  const int n = (int)ncols;
+  QrMaps mp;
+  STATUS_TRY(make_role_map(h, &mp.vA_t, V, h->n_r, n, ldv, ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &mp.vA_nt, V, h->n_r, n, ldv, ROLE_A_NOTRANS));
+  STATUS_TRY(make_role_map(h, &mp.vX, V, h->n_r, n, ldv, ROLE_X));
+  STATUS_TRY(make_role_map(h, &mp.gA_t, h->Gws, n, n, pad_ld(n), ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &mp.gX, h->Gws, n, n, pad_ld(n), ROLE_X));
+
+  // Alg.4: est > 1e8 -> shifted CholeskyQR2; est < 20 -> CholeskyQR; else CholeskyQR2
+  int variant = cond_est > 1e8 ? CHASE_QR_SHIFTED : (cond_est < 20.0 ? CHASE_QR_CHOL1 : CHASE_QR_CHOL2);
+  int info = 0, passes = 0;
+  chase_status_t st = CHASE_OK;
+  if (variant != CHASE_QR_SHIFTED) {
+    const int rounds = variant == CHASE_QR_CHOL1 ? 1 : 2;
+    for (int i = 0; i < rounds; ++i) {
+      st = cholqr_pass(h, V, ldv, n, false, mp, &info);
+      if (st != CHASE_OK) break;
+      ++passes;
+    }
+    if (st == CHASE_ECHOL && passes == 0) {     // reading #14: escalate, V untouched
+      variant = CHASE_QR_SHIFTED;
+      st = CHASE_OK;
+    }
+  }
+  if (variant == CHASE_QR_SHIFTED && st == CHASE_OK && passes == 0) {
+    st = cholqr_pass(h, V, ldv, n, true, mp, &info);
+    if (st == CHASE_OK) {
+      ++passes;
+      for (int i = 0; i < 2 && st == CHASE_OK; ++i) {
+        st = cholqr_pass(h, V, ldv, n, false, mp, &info);
+        if (st == CHASE_OK) ++passes;
+      }
+    }
+  }
+  if (stats) {
+    stats->qr_variant = variant;
+    stats->qr_passes = passes;
+  }
+  if (info_out) *info_out = info;
+  return st;
+}
+
+double chase_shift_value(int64_t m, int64_t n, double norm) {
+  return 11.0 * (double)(m * n + n * (n + 1)) * 1.1102230246251565e-16 * norm;
+}
+
+double chase_cond_est(const double* ritz, int64_t n, double c, double e, const int32_t* degrees,
+                      int64_t locked) {
+  if (!ritz || !degrees || n < 1 || locked < 0 || locked >= n || !(e > 0.0)) return NAN;
+  const double tp = (ritz[0] - c) / e;
+  const double t = (ritz[locked] - c) / e;
+  // |rho| = max |t -+ sqrt(t^2 - 1)|: for |t| <= 1 both roots have modulus 1
+  auto rho = [](double x) { return std::fabs(x) <= 1.0 ? 1.0 : std::fabs(x) + std::sqrt(x * x - 1.0); };
+  const int32_t d = degrees[locked];
+  int32_t dM = d;
+  for (int64_t j = locked; j < n; ++j) dM = std::max(dM, degrees[j]);
+  return std::pow(rho(t), (double)d) * std::pow(rho(tp), (double)(dM - d));
+}
+
+chase_status_t chase_profile_enable(chase_handle_t h, int enable) {
+  if (!h) return CHASE_EINVAL;
+  h->profiling = enable != 0;
+  return CHASE_OK;
+}
+
+chase_status_t chase_profile_read(chase_handle_t h, double ms[6], int64_t launches[6]) {
+  if (!h || !ms || !launches) return CHASE_EINVAL;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < CAT_N; ++i) ms[i] = 0.0;
+  for (auto& ev : h->evs) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, ev.a, ev.b));
+    ms[ev.cat] += t;
+    h->pool.push_back(ev.a);
+    h->pool.push_back(ev.b);
+  }
+  h->evs.clear();
+  for (int i = 0; i < CAT_N; ++i) {
+    launches[i] = h->launches[i];
+    h->launches[i] = 0;
+  }
+  return CHASE_OK;
+}
+
+chase_status_t chase_destroy(chase_handle_t h) {
+  if (!h) return CHASE_EINVAL;
+  if (h->rcomm) ncclCommDestroy(h->rcomm);
+  if (h->ccomm) ncclCommDestroy(h->ccomm);
+  if (h->world) ncclCommDestroy(h->world);
+  for (auto& ev : h->evs) {
+    cudaEventDestroy(ev.a);
+    cudaEventDestroy(ev.b);
+  }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->h_info) cudaFreeHost(h->h_info);
+  delete h;
+  return CHASE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// dgemm.cuh -- real-double tensor-core GEMM with the fused Chebyshev-recurrence epilogue, the
+// real-symmetric counterpart of zgemm.cuh (SYMM of the filter for real problems, P:76
+// "templated for complex/real type"; BASELINE config C5).
+//
+//   out[m, n] = alpha * ( sum_k opA[m, k] * X[k, n] - c * band(xin)[m, n] ) + beta * out[m, n]
+//
+// Same pipeline as zgemm (TMA + 128B swizzle, mbarrier ring refilled by thread 0, 8 DMMA
+// warps).  Tiles: 128 x 128 outputs per CTA, 16 k per stage (one 128-byte row),
+// 32 x 64 per warp.  Inside each stage the four m16n8k4 sub-steps h use the XOR-linear k
+// permutation k = (t&1 ? 3 : 0) ^ (t&2 ? 12 : 0) ^ (h&1 ? 1 : 0) ^ (h&2 ? 4 : 0)
+// (t = lane%4), chosen by exhaustive search so every 64-bit fragment load of A, A^T and X is
+// bank-conflict free under the swizzle.
+#pragma once
+#include "common.cuh"
+
+namespace chase {
+
+constexpr int DG_BM = 128;
+constexpr int DG_BN = 128;
+constexpr int DG_BK = 16;
+constexpr int DG_STAGES = 6;
+constexpr int DG_CONSUMERS = 8;   // 4 along M x 2 along N
+constexpr int DG_THREADS = DG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
+constexpr int DG_A_BYTES = DG_BM * DG_BK * 8;   // 16 KB
+constexpr int DG_X_BYTES = DG_BN * DG_BK * 8;   // 16 KB
+constexpr int DG_STAGE_BYTES = DG_A_BYTES + DG_X_BYTES;
+constexpr int DG_SMEM_BYTES = DG_STAGES * DG_STAGE_BYTES + 1024 + 2 * DG_STAGES * 8;
+
+struct DGemmArgs {
+  int M, N, K;
+  int a_d0, a_d1;
+  int x_k0, x_n0;
+  double* out;
+  long long ldo;
+  const double* xin;
+  long long ldx;
+  double alpha, beta, c;
+  int use_beta;
+  int band_lo, band_hi;
+  int band_shift;
+  int upper_only;
+  const int* abort_flag;
+};
+
+__device__ __forceinline__ int dg_kperm(int t, int h) {
+  return ((t & 1) ? 3 : 0) ^ ((t & 2) ? 12 : 0) ^ ((h & 1) ? 1 : 0) ^ ((h & 2) ? 4 : 0);
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(DG_THREADS, 1)
+    dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                 const DGemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DG_STAGES * DG_STAGE_BYTES);
+  uint64_t* empty = full + DG_STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * DG_BM, n0 = blockIdx.x * DG_BN;
+  if (g.upper_only && m0 > n0 + DG_BN - 1) return;
+  if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
+  const int KT = (g.K + DG_BK - 1) / DG_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], DG_CONSUMERS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // stage `s` <- k-tile `kt` (TMA, completion on full[s]); issued by thread 0 only
+  auto issue = [&](int kt, int s) {
+    mbar_arrive_expect_tx(&full[s], DG_STAGE_BYTES);
+    uint8_t* sa = smem + s * DG_STAGE_BYTES;
+    uint8_t* sx = sa + DG_A_BYTES;
+    const int k0 = kt * DG_BK;
+    if (TRANS) {
+      tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);     // box 16 k x 128 m
+    } else {
+#pragma unroll
+      for (int b = 0; b < DG_BM / 16; ++b)                      // box 16 m x 16 k
+        tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+    }
+    tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);       // box 16 k x 128 n
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmX);
+    for (int kt = 0; kt < DG_STAGES && kt < KT; ++kt) issue(kt, kt);
+  }
+
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc[2][8][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % DG_STAGES;
+    mbar_wait(&full[s], (kt / DG_STAGES) & 1);
+    const uint8_t* sa = smem + s * DG_STAGE_BYTES;
+    const uint8_t* sx = sa + DG_A_BYTES;
+    const bool tail = (kt == KT - 1) && (g.K - kt * DG_BK < DG_BK);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int k = dg_kperm(tq, h);
+      double a[2][2], b[8];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int m = wm * 32 + mt * 16 + r * 8 + gq;
+          const int off = TRANS ? m * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3))
+                                : (m >> 4) * 2048 + k * 128 +
+                                      (((((m & 15) >> 1) ^ (k & 7)) << 4) | ((m & 1) << 3));
+          a[mt][r] = *reinterpret_cast<const double*>(sa + off);
+        }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int n = wn * 64 + nt * 8 + gq;
+        b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
+      }
+      if (tail && kt * DG_BK + k >= g.K) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) a[mt][0] = a[mt][1] = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) b[nt] = 0.0;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill the stage released one iteration ago (most likely already drained by all warps)
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + DG_STAGES < KT) {
+      const int sp = (kt - 1) % DG_STAGES;
+      mbar_wait(&empty[sp], ((kt - 1) / DG_STAGES) & 1);
+      issue(kt - 1 + DG_STAGES, sp);
+    }
+  }
+
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * 64 + nt * 8 + 2 * tq + (r & 1);
+        if (row < g.M && col < g.N) {
+          double v = acc[mt][nt][r];
+          if (row >= g.band_lo && row < g.band_hi)
+            v -= g.c * g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+          v *= g.alpha;
+          double* o = g.out + (long long)row + (long long)col * g.ldo;
+          if (g.use_beta) v += g.beta * *o;
+          *o = v;
+        }
+      }
+}
+
+}  // namespace chase

@@ -1,0 +1,161 @@
+// qr_kernels.cuh -- the latency-bound pieces of 1D-CholeskyQR (Alg.3; Alg.4 l.5-7,
+// P:294-297) for complex double.  The flop-heavy pieces (Gram X^H X, the trailing HERK update
+// of the blocked POTRF and the TRSM right-looking updates) run on the tensor-core zgemm.
+//
+//   potrf_diag_kernel    unblocked upper Cholesky of one nb x nb diagonal block, in smem
+//   potrf_panel_kernel   R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:]   (forward substitution)
+//   trsm_diag_kernel     X[:, kb:kb+nb] = X[:, kb:kb+nb] R_kk^{-1}  (one thread per row)
+//   shift_kernel         norm = Re tr(G) (= ||X||_F^2, reading #12); s = 11(mn+n(n+1)) u norm;
+//                        G += s I
+// A POTRF failure (radicand <= 0 or NaN) writes the 1-based global pivot into *info once;
+// every later kernel of the same factorisation sees *info != 0 and returns.
+#pragma once
+#include "common.cuh"
+
+namespace chase {
+
+constexpr int QR_NB = 32;   // diagonal block size of the blocked POTRF / TRSM
+
+// scalar ops for T = double (real symmetric) or double2 (complex Hermitian)
+__device__ __forceinline__ double2 s_mul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double s_mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double2 s_cmul(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double s_cmul(double a, double b) { return a * b; }
+__device__ __forceinline__ double2 s_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double s_sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double2 s_div(double2 a, double r) { return make_double2(a.x / r, a.y / r); }
+__device__ __forceinline__ double s_div(double a, double r) { return a / r; }
+__device__ __forceinline__ double s_re(double2 a) { return a.x; }
+__device__ __forceinline__ double s_re(double a) { return a; }
+template <typename T> __device__ __forceinline__ T s_real(double r);
+template <> __device__ __forceinline__ double2 s_real<double2>(double r) { return make_double2(r, 0.0); }
+template <> __device__ __forceinline__ double s_real<double>(double r) { return r; }
+__device__ __forceinline__ void s_add_re(double2& a, double v) { a.x += v; }
+__device__ __forceinline__ void s_add_re(double& a, double v) { a += v; }
+
+// One CTA.  G column-major (ld), block rows/cols [kb, kb+nb).  On exit the upper triangle of
+// the block holds R_kk (real positive diagonal).  Unblocked right-looking Cholesky in smem.
+template <typename T>
+__global__ void potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info) {
+  __shared__ T S[QR_NB][QR_NB + 1];   // S[a][b] = G[kb+a, kb+b]
+  if (*info != 0) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int idx = tid; idx < nb * nb; idx += nt) {
+    const int a = idx % nb, b = idx / nb;
+    S[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    const double d = s_re(S[j][j]);
+    if (!(d > 0.0)) {                       // uniform: every thread reads the same d
+      if (tid == 0) atomicCAS(info, 0, kb + j + 1);
+      return;
+    }
+    const double r = sqrt(d);
+    __syncthreads();
+    for (int l = j + 1 + tid; l < nb; l += nt) S[j][l] = s_div(S[j][l], r);
+    if (tid == 0) S[j][j] = s_real<T>(r);
+    __syncthreads();
+    // trailing update of the upper triangle: S[a][b] -= conj(R[j][a]) R[j][b], j < a <= b
+    const int w = nb - j - 1;
+    for (int idx = tid; idx < w * w; idx += nt) {
+      const int a = j + 1 + idx % w, b = j + 1 + idx / w;
+      if (a <= b) S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], S[j][b]));
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < nb * nb; idx += nt) {
+    const int a = idx % nb, b = idx / nb;
+    if (a <= b) G[(long long)(kb + a) + (long long)(kb + b) * ld] = S[a][b];
+  }
+}
+
+// R_kk^H Y = G[kb:kb+nb, kb+nb:n]: one thread per column, R_kk broadcast from smem, the column
+// kept in smem laid out [row][thread] (conflict free).
+constexpr int PANEL_THREADS = 128;
+template <typename T>
+constexpr int panel_smem() { return (QR_NB * QR_NB + QR_NB * PANEL_THREADS) * (int)sizeof(T); }
+template <typename T>
+__global__ void __launch_bounds__(PANEL_THREADS)
+    potrf_panel_kernel(T* G, long long ld, int kb, int nb, int n, const int* info) {
+  extern __shared__ __align__(16) unsigned char qr_dyn[];
+  T (*R)[QR_NB] = reinterpret_cast<T (*)[QR_NB]>(qr_dyn);
+  T (*Y)[PANEL_THREADS] = reinterpret_cast<T (*)[PANEL_THREADS]>(qr_dyn + QR_NB * QR_NB * sizeof(T));
+  if (*info != 0) return;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nb * nb; idx += PANEL_THREADS) {
+    const int a = idx % nb, b = idx / nb;
+    R[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
+  }
+  const int col = kb + nb + blockIdx.x * PANEL_THREADS + tid;
+  const bool active = col < n;
+  if (active)
+    for (int a = 0; a < nb; ++a) Y[a][tid] = G[(long long)(kb + a) + (long long)col * ld];
+  __syncthreads();
+  if (!active) return;
+  for (int a = 0; a < nb; ++a) {
+    T acc = Y[a][tid];
+    for (int b = 0; b < a; ++b) acc = s_sub(acc, s_cmul(R[b][a], Y[b][tid]));  // (R^H)[a][b]
+    acc = s_div(acc, s_re(R[a][a]));
+    Y[a][tid] = acc;
+    G[(long long)(kb + a) + (long long)col * ld] = acc;
+  }
+}
+
+// X[:, kb:kb+nb] <- X[:, kb:kb+nb] R_kk^{-1}, R_kk = upper block of G.  One thread per row:
+//   y_l = (x_l - sum_{k<l} y_k R[k][l]) / R[l][l].
+constexpr int TRSM_THREADS = 128;
+template <typename T>
+constexpr int trsm_smem() { return (QR_NB * QR_NB + QR_NB * TRSM_THREADS) * (int)sizeof(T); }
+template <typename T>
+__global__ void __launch_bounds__(TRSM_THREADS)
+    trsm_diag_kernel(T* X, long long ldx, int m, const T* G, long long ld, int kb, int nb) {
+  extern __shared__ __align__(16) unsigned char qr_dyn[];
+  T (*R)[QR_NB] = reinterpret_cast<T (*)[QR_NB]>(qr_dyn);
+  T (*Y)[TRSM_THREADS] = reinterpret_cast<T (*)[TRSM_THREADS]>(qr_dyn + QR_NB * QR_NB * sizeof(T));
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nb * nb; idx += TRSM_THREADS) {
+    const int a = idx % nb, b = idx / nb;
+    R[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
+  }
+  const long long row = (long long)blockIdx.x * TRSM_THREADS + tid;
+  const bool active = row < m;
+  if (active)
+    for (int l = 0; l < nb; ++l) Y[l][tid] = X[row + (long long)(kb + l) * ldx];
+  __syncthreads();
+  if (!active) return;
+  for (int l = 0; l < nb; ++l) {
+    T acc = Y[l][tid];
+    for (int k = 0; k < l; ++k) acc = s_sub(acc, s_mul(Y[k][tid], R[k][l]));
+    acc = s_div(acc, s_re(R[l][l]));
+    Y[l][tid] = acc;
+    X[row + (long long)(kb + l) * ldx] = acc;
+  }
+}
+
+// Alg.4 l.5-7 on the reduced Gram matrix: norm = sum_j Re G[j][j]; s = 11 (m n + n (n+1)) u norm;
+// G[j][j] += s.  One CTA of 256 threads, fixed-order reduction (deterministic).
+template <typename T>
+__global__ void shift_kernel(T* G, long long ld, int n, long long m_global, double* s_out) {
+  __shared__ double part[256];
+  const int tid = threadIdx.x;
+  double acc = 0.0;
+  for (int j = tid; j < n; j += 256) acc += s_re(G[(long long)j + (long long)j * ld]);
+  part[tid] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) part[tid] += part[tid + w];
+    __syncthreads();
+  }
+  const double norm = part[0];
+  const double u = 1.1102230246251565e-16;   // 2^-53
+  const double s = 11.0 * (double)(m_global * (long long)n + (long long)n * (n + 1)) * u * norm;
+  for (int j = tid; j < n; j += 256) s_add_re(G[(long long)j + (long long)j * ld], s);
+  if (tid == 0 && s_out != nullptr) *s_out = s;
+}
+
+}  // namespace chase

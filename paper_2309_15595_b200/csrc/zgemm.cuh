@@ -1,0 +1,200 @@
+// zgemm.cuh -- complex-double tensor-core GEMM with the Chebyshev-recurrence epilogue fused
+// (the HEMM of the filter; also the Gram / trailing updates of CholeskyQR, Alg.3).
+//
+//   out[m, n] = alpha * ( sum_k opA[m, k] * X[k, n]  -  c * band(xin)[m, n] ) + beta * out[m, n]
+//
+// opA = A (NoTrans, even filter steps "H^H B -> C") or A^H (ConjTrans, odd steps "H C -> B",
+// P:149), A read through a TMA tensor map, never modified.  band(xin) is non-zero only on rows
+// [band_lo, band_hi) -- the diagonal rows of -cI this rank owns (reading #6); the beta term is
+// applied only when use_beta (designated rank, reading #7; never on step 1 so B is never read
+// before it is written).
+//
+// B200 design: FP64 has no tcgen05 kind, so the math runs on the FP64 tensor pipe through
+// warp-level DMMA (mma.sync.m16n8k4.f64, 37.1 TFLOP/s measured).  Operand tiles are staged by
+// TMA (cp.async.bulk.tensor, SWIZZLE_128B) into an 8-stage mbarrier ring; thread 0 issues the
+// TMA loads in-line (a 9th producer warp would put 3 warps on one SM sub-partition and cap
+// registers at 168 -> spills); 8 DMMA warps each own a 32x32 complex sub-tile (the complex
+// product is split into 4 real DMMA products, 8 real flops per complex MAC).
+// The k index inside each 8-wide smem row is permuted (k = 2t + h for mma sub-step h) so every
+// 128-bit fragment load of A, A^H and X is bank-conflict free under the 128-byte swizzle.
+#pragma once
+#include "common.cuh"
+
+namespace chase {
+
+constexpr int ZG_BM = 128;        // rows of out per CTA
+constexpr int ZG_BN = 64;         // columns of out per CTA
+constexpr int ZG_BK = 8;          // complex k per stage (one 128-byte swizzle row)
+constexpr int ZG_STAGES = 8;
+constexpr int ZG_CONSUMERS = 8;   // consumer warps (4 along M x 2 along N)
+constexpr int ZG_THREADS = ZG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
+constexpr int ZG_A_BYTES = ZG_BM * ZG_BK * 16;   // 16 KB
+constexpr int ZG_X_BYTES = ZG_BN * ZG_BK * 16;   // 8 KB
+constexpr int ZG_STAGE_BYTES = ZG_A_BYTES + ZG_X_BYTES;
+constexpr int ZG_SMEM_BYTES = ZG_STAGES * ZG_STAGE_BYTES + 1024 + 2 * ZG_STAGES * 8;
+
+struct ZGemmArgs {
+  int M, N, K;
+  int a_d0, a_d1;          // tensor-map coordinate offsets of opA's (0,0) element, in complex
+                           // elements: NoTrans (row = m, col = k), ConjTrans (row = k, col = m)
+  int x_k0, x_n0;          // X tensor-map offsets (row = k, col = n)
+  double2* out;            // out(m, n) = out[m + n * ldo]
+  long long ldo;
+  const double2* xin;      // band input: xin(row, n) = xin[row + n * ldx]
+  long long ldx;
+  double alpha, beta, c;
+  int use_beta;
+  int band_lo, band_hi;    // out rows [band_lo, band_hi) subtract c * xin[row + band_shift, n]
+  int band_shift;
+  int upper_only;          // skip CTAs whose tile lies strictly below the diagonal (m > n)
+  const int* abort_flag;   // non-null: skip the whole GEMM when *abort_flag != 0 (POTRF info)
+};
+
+template <bool CONJ>
+__global__ void __launch_bounds__(ZG_THREADS, 1)
+    zgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                 const ZGemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
+  uint64_t* empty = full + ZG_STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * ZG_BM, n0 = blockIdx.x * ZG_BN;
+  if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
+  if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
+  const int KT = (g.K + ZG_BK - 1) / ZG_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ZG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ZG_CONSUMERS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // stage `s` <- k-tile `kt` (TMA, completion on full[s]); issued by thread 0 only
+  auto issue = [&](int kt, int s) {
+    mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
+    uint8_t* sa = smem + s * ZG_STAGE_BYTES;
+    uint8_t* sx = sa + ZG_A_BYTES;
+    const int k0 = kt * ZG_BK;
+    if (CONJ) {
+      // opA[m][k] = conj(A[k][m]); A rows (k) contiguous: one 128 x 8 box, row = m
+      tma_load_2d(sa, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
+    } else {
+      // A rows (m) contiguous: 16 boxes of 8 m x 8 k, box b holds rows [8b, 8b+8), row = k
+#pragma unroll
+      for (int b = 0; b < ZG_BM / 8; ++b)
+        tma_load_2d(sa + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+    }
+    tma_load_2d(sx, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmX);
+    for (int kt = 0; kt < ZG_STAGES && kt < KT; ++kt) issue(kt, kt);
+  }
+
+  // -------------------------------------------------------------- consumer warps
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc_re[2][4][4], acc_im[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % ZG_STAGES;
+    mbar_wait(&full[s], (kt / ZG_STAGES) & 1);
+    const uint8_t* sa = smem + s * ZG_STAGE_BYTES;
+    const uint8_t* sx = sa + ZG_A_BYTES;
+    const bool tail = (kt == KT - 1) && (g.K - kt * ZG_BK < ZG_BK);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = 2 * tq + h;
+      double2 a[2][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int m = wm * 32 + mt * 16 + r * 8 + gq;  // m & 7 == gq
+          const int off = CONJ ? m * 128 + ((k ^ gq) << 4)
+                               : (m >> 3) * 1024 + k * 128 + ((gq ^ k) << 4);
+          a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
+        }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int n = wn * 32 + nt * 8 + gq;
+        b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
+      }
+      if (tail && kt * ZG_BK + k >= g.K) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) a[mt][0] = a[mt][1] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = make_double2(0.0, 0.0);
+      }
+      // real parts of opA times X
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          dmma_16x8x4(acc_re[mt][nt], a[mt][0].x, a[mt][1].x, b[nt].x);
+          dmma_16x8x4(acc_im[mt][nt], a[mt][0].x, a[mt][1].x, b[nt].y);
+        }
+      // imaginary parts: A: re -= Ai*Bi, im += Ai*Br;  A^H: re += Ai*Bi, im -= Ai*Br
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const double bre = CONJ ? b[nt].y : -b[nt].y;
+          const double bim = CONJ ? -b[nt].x : b[nt].x;
+          dmma_16x8x4(acc_re[mt][nt], a[mt][0].y, a[mt][1].y, bre);
+          dmma_16x8x4(acc_im[mt][nt], a[mt][0].y, a[mt][1].y, bim);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill the stage released one iteration ago (most likely already drained by all warps)
+    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + ZG_STAGES < KT) {
+      const int sp = (kt - 1) % ZG_STAGES;
+      mbar_wait(&empty[sp], ((kt - 1) / ZG_STAGES) & 1);
+      issue(kt - 1 + ZG_STAGES, sp);
+    }
+  }
+
+  // -------------------------------------------------------------- fused recurrence epilogue
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * 32 + nt * 8 + 2 * tq + (r & 1);
+        if (row < g.M && col < g.N) {
+          double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
+          if (row >= g.band_lo && row < g.band_hi) {
+            const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+            vr -= g.c * x.x;
+            vi -= g.c * x.y;
+          }
+          vr *= g.alpha;
+          vi *= g.alpha;
+          double2* o = g.out + (long long)row + (long long)col * g.ldo;
+          if (g.use_beta) {
+            const double2 old = *o;
+            vr += g.beta * old.x;
+            vi += g.beta * old.y;
+          }
+          *o = make_double2(vr, vi);
+        }
+      }
+}
+
+}  // namespace chase

@@ -1,0 +1,114 @@
+"""GPU parity of chase_filter (C-ABI, libchase.so) against the CPU oracle on the same seeded
+inputs.  Tolerance: relative Frobenius error <= 1e-10 for degree <= 20 (BASELINE north star),
+applied per column; bookkeeping bit-exact."""
+import numpy as np
+import pytest
+
+import chase_inputs as ci
+import oracle
+import paper_2309_15595_b200 as cb
+from gpu_util import colwise_rel, dev, host
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def make_problem(N, n, complex_, seed, spectrum="uniform"):
+    lam = ci.uniform_spectrum(N) if spectrum == "uniform" else ci.clement_spectrum(N)
+    A = ci.dense_from_spectrum(lam, seed, complex_)
+    V0 = ci.gaussian_block(N, n, seed + 1000, complex_)
+    b = ci.bounds_from_spectrum(lam, n)
+    return A, V0, b
+
+
+def gpu_filter(A, V0, degrees, b, complex_, ldv=None, poison=False):
+    import torch
+    N, n = V0.shape
+    h = cb.Chase(cb.CHASE_C128 if complex_ else cb.CHASE_R64, N, n)
+    if poison:
+        h.ws.fill_(0xFF)            # NaN bit patterns: B must never be read before written
+    Ad = dev(A)
+    Vd = dev(V0, ld=ldv)
+    A_before = Ad.clone()
+    st = h.filter(Ad, Vd, degrees, b.c, b.e, (b.mu_1, b.mu_ne, b.b_sup))
+    torch.cuda.synchronize()
+    assert torch.equal(Ad, A_before), "A_local must not be modified"
+    rec = h.record()
+    out = host(Vd)
+    h.close()
+    return out, st, rec
+
+
+RAGGED = [2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20]
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("N,n,degrees", [
+    (61, 17, RAGGED),
+    (300, 7, [20] * 7),
+    (512, 60, [20] * 60),            # config C1
+    (257, 129, [2] * 40 + [10] * 49 + [20] * 40),
+    (130, 1, [8]),
+    (200, 70, list(ci.ramp_degrees(70, 10, 20))),
+])
+def test_filter_matches_oracle(complex_, N, n, degrees):
+    A, V0, b = make_problem(N, n, complex_, seed=N + n)
+    ref, _ = oracle.chebyshev_filter(A, V0, degrees, b.c, b.e, b.mu_1)
+    out, st, (rec, mv) = gpu_filter(A, V0, degrees, b, complex_)
+    assert colwise_rel(out, ref) <= TOL
+    orec, omv = oracle.filter_record(degrees, N, N)
+    assert rec == orec and mv == omv == st["matvecs"]
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+def test_filter_degree36_clement(complex_):
+    A, V0, b = make_problem(160, 24, complex_, seed=5, spectrum="clement")
+    degs = [36] * 24
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    out, _, _ = gpu_filter(A, V0, degs, b, complex_)
+    assert colwise_rel(out, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+def test_nan_poisoned_workspace_and_padded_ld(complex_):
+    A, V0, b = make_problem(100, 9, complex_, seed=3)
+    degs = [4, 4, 6, 6, 6, 10, 12, 12, 20]
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    out, _, _ = gpu_filter(A, V0, degs, b, complex_, ldv=128, poison=True)
+    assert np.all(np.isfinite(out))
+    assert colwise_rel(out, ref) <= TOL
+
+
+def test_argument_errors_leave_V_untouched():
+    import torch
+    A, V0, b = make_problem(64, 4, True, seed=9)
+    h = cb.Chase(cb.CHASE_C128, 64, 4)
+    Ad, Vd = dev(A), dev(V0)
+    V_before = Vd.clone()
+    bounds = (b.mu_1, b.mu_ne, b.b_sup)
+    for degs, c, e, status in [([2, 3, 4, 4], b.c, b.e, 2), ([4, 2, 4, 4], b.c, b.e, 2),
+                               ([0, 2, 2, 2], b.c, b.e, 2), ([2, 2, 2, 2], b.c, -1.0, 3),
+                               ([2, 2, 2, 2], b.c, b.e, None)]:
+        if status is None:
+            # mu_1 inside the damped interval
+            with pytest.raises(cb.ChaseError) as ei:
+                h.filter(Ad, Vd, degs, b.c, b.e, (b.c, b.mu_ne, b.b_sup))
+            assert ei.value.status == 3
+            continue
+        with pytest.raises(cb.ChaseError) as ei:
+            h.filter(Ad, Vd, degs, c, e, bounds)
+        assert ei.value.status == status
+    with pytest.raises(cb.ChaseError) as ei:
+        h.filter(Ad, Vd, [2] * 5, b.c, b.e, bounds, ncols=5)      # ncols > n_max
+    assert ei.value.status == 1
+    torch.cuda.synchronize()
+    assert torch.equal(Vd, V_before)
+    h.close()
+
+
+def test_repeatable_bitwise():
+    A, V0, b = make_problem(200, 33, True, seed=17)
+    d = [20] * 33
+    o1, _, _ = gpu_filter(A, V0, d, b, True)
+    o2, _, _ = gpu_filter(A, V0, d, b, True)
+    assert np.array_equal(o1, o2)
