@@ -1,0 +1,401 @@
+"""Benchmark of the ChASE hot path on B200: one step = chase_filter (Chebyshev filter, degree
+20 on every vector) + chase_cholqr (Alg.4-selected CholeskyQR variant) on the resident
+synthetic workload, through the C-ABI (libchase.so).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2|C3|C4|C5|auto]
+    torchrun --nproc-per-node N bench.py --gpus N ...            (N > 1, one rank per GPU)
+    python bench.py --impl reference ...                         (CPU oracle arm)
+
+Workloads (BASELINE.json configs, synthetic, seeded):
+    N=1  C2: N=30000 complex Hermitian, Uniform spectrum, nev=2250 nex=750, degree 20, 1x1
+    N=2  weak-scaling point of C2 (paper Fig.3a recipe, N = 30000 sqrt(P)): N=42426, n=3000, 2x1
+    N=4  N=60000, n=3000, 2x2
+    N=8  C4: N=120000 complex Uniform, nev=1200 nex=400, degree 20, 2x4 (north-star target)
+Metric (BASELINE.json): Chebyshev filter FP64 TFLOP/s (max over ranks): algorithmic filter
+flops 8 N^2 sum_j d_j (complex; 2 N^2 sum d real) divided by the whole step time (filter +
+QR), so QR time is charged against the filter number (conservative).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Chebyshev filter FP64 TFLOP/s (max over ranks) at 1/2/4/8 B200; % of FP64 peak"
+# FP64 tensor (DMMA) peak measured on this pool's B200 by tools/microbench/fp64_peak.cu
+# (profiles/r01/fp64_peak.log: 37.1 TFLOP/s burst and sustained at 1965 MHz).
+# MEASURED_PEAKS.json carries no FP64 figure.
+FP64_PEAK_TFLOPS = 37.1
+GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}
+
+
+def workload(n_gpus: int, name: str):
+    import chase_inputs as ci
+    if name == "auto":
+        name = {1: "C2", 8: "C4"}.get(n_gpus, "W")
+    if name == "W":   # weak-scaling point of C2 (N grows with sqrt(#GPUs))
+        N = int(round(30000 * math.sqrt(n_gpus)))
+        return dict(name=f"W{n_gpus}", N=N, nev=2250, nex=750, complex_=True, spectrum="uniform",
+                    seed=2, degree=20,
+                    desc=f"C2 weak-scaling point: N={N} complex Hermitian Uniform, nev=2250 nex=750, "
+                         f"degree 20")
+    c = ci.CONFIGS[name]
+    deg = "ramp 10-36" if c.degree is None else f"degree {c.degree}"
+    return dict(name=name, N=c.N, nev=c.nev, nex=c.nex, complex_=c.complex_, spectrum=c.spectrum,
+                seed=c.seed, degree=c.degree,
+                desc=f"{name}: N={c.N} {'complex Hermitian' if c.complex_ else 'real symmetric'} "
+                     f"{c.spectrum.capitalize()}, nev={c.nev} nex={c.nex}, {deg}")
+
+
+def spectrum(w):
+    import chase_inputs as ci
+    if w["spectrum"] == "uniform":
+        return ci.uniform_spectrum(w["N"])
+    if w["spectrum"] == "clement":
+        return ci.clement_spectrum(w["N"])
+    return ci.wilkinson_spectrum(w["N"])
+
+
+def degrees_of(w):
+    import chase_inputs as ci
+    n = w["nev"] + w["nex"]
+    return ci.uniform_degrees(n, w["degree"]) if w["degree"] else ci.ramp_degrees(n)
+
+
+def generator(w, lam):
+    import chase_inputs as ci
+    return ci.dft_phase(lam, w["seed"]) if w["complex_"] else ci.hartley_sign(lam, w["seed"])
+
+
+def filter_flops(w, degrees):
+    return (8.0 if w["complex_"] else 2.0) * float(w["N"]) ** 2 * float(np.sum(degrees))
+
+
+def qr_flops(w, n, passes):
+    # per pass: Gram (upper half, 4 N n^2 real flops complex) + TRSM (4 N n^2) + POTRF (4n^3/3)
+    f = 8.0 * w["N"] * n * n + 4.0 * n ** 3 / 3.0
+    return passes * (f if w["complex_"] else f / 4.0)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.index)], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                pw.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "power_w_max": max(pw),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ====================================================================== CPU oracle (baseline)
+def oracle_sample(A_host, V0_host, degrees, b, cols):
+    """Time the oracle filter (oracle/filter.py, as it stands) on `cols` columns of the same
+    workload (full A).  Returns (seconds, flops)."""
+    import oracle
+    V = np.asfortranarray(V0_host[:, :cols])
+    d = list(int(x) for x in degrees[:cols])
+    t0 = time.perf_counter()
+    oracle.chebyshev_filter(A_host, V, d, b.c, b.e, b.mu_1)
+    t = time.perf_counter() - t0
+    N = A_host.shape[0]
+    return t, (8.0 if np.iscomplexobj(A_host) else 2.0) * N * N * sum(d)
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the box's host cores, on a bounded sample of the
+    same workload (one column of V per step, full degree, full A)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import chase_inputs as ci
+    n_gpus = args.gpus
+    w = workload(n_gpus, args.config)
+    if w["N"] > 60000:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"oracle needs the full {w['N']}^2 matrix in host memory ({16 * w['N'] ** 2 / 1e9:.0f} GB)"}))
+        return
+    lam = spectrum(w)
+    n = w["nev"] + w["nex"]
+    degrees = degrees_of(w)
+    b = ci.bounds_from_spectrum(lam, n)
+    gen = generator(w, lam)
+    torch.set_num_threads(cores())
+    A = gen.block(0, w["N"], 0, w["N"], device="cpu").numpy().T      # host, column-major
+    V0 = ci.gaussian_block(w["N"], n, w["seed"] + 1000, w["complex_"])
+    for _ in range(args.warmup):
+        oracle_sample(A, V0, degrees, b, 1)
+    ts, fl = [], 0.0
+    for _ in range(args.steps):
+        t, f = oracle_sample(A, V0, degrees, b, 1)
+        ts.append(t)
+        fl += f
+    tot = sum(ts)
+    value = fl / tot / 1e12
+    sample = (f"oracle.chebyshev_filter on 1 of {n} columns per step (degree {int(degrees[0])}), "
+              f"full {w['N']}x{w['N']} A, numpy matmul")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": w["desc"], "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ====================================================================== GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="auto")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-cols", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import chase_inputs as ci
+    import paper_2309_15595_b200 as cb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p, q = GRIDS[n_gpus]
+    myrow, mycol = rank // q, rank % q
+
+    w = workload(n_gpus, args.config)
+    N, n = w["N"], w["nev"] + w["nex"]
+    lam = spectrum(w)
+    degrees = degrees_of(w)
+    b = ci.bounds_from_spectrum(lam, n)
+    bounds = (b.mu_1, b.mu_ne, b.b_sup)
+    est = cb.chase_cond_est(lam, b.c, b.e, degrees, 0)
+    dtype = cb.CHASE_C128 if w["complex_"] else cb.CHASE_R64
+    tdt = torch.complex128 if w["complex_"] else torch.float64
+
+    uid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(cb.chase_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+    stream = torch.cuda.current_stream(dev)
+    h = cb.Chase(dtype, N, n, p, q, myrow, mycol, uid, local, stream)
+    n_r, n_c, r0, c0 = h.n_r, h.n_c, h.r0, h.c0
+
+    # ---- inputs, resident in HBM before the timed region
+    gen = generator(w, lam)
+    A_t = gen.block(r0, n_r, c0, n_c, device=dev)                 # (n_c, n_r) storage
+    A_local = A_t.T                                               # column-major n_r x n_c view
+    V0_full = ci.gaussian_block(N, n, w["seed"] + 1000, w["complex_"])
+    V0_rows = np.asfortranarray(V0_full[r0:r0 + n_r])
+    del V0_full
+    V0_host = torch.from_numpy(np.ascontiguousarray(V0_rows.T)).pin_memory()   # (n, n_r) pinned
+    V_t = V0_host.to(dev)                                         # (n, n_r) storage
+    V = V_t.T
+    out_host = torch.empty_like(V0_host).pin_memory()
+    torch.cuda.synchronize()
+
+    def step():
+        h.filter(A_local, V, degrees, b.c, b.e, bounds)
+        return h.cholqr(V, est)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    qr_info = None
+    for _ in range(args.warmup):
+        qr_info = step()
+    barrier()
+
+    # ---- timed region (device-resident inputs); A (>= 14 GB) is larger than L2
+    clocks = Clocks(local)
+    cb.chase_profile_enable(h.h, True)
+    cb.chase_profile_read(h.h)                      # reset counters
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        qr_info = step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1)
+    prof_ms, prof_n = cb.chase_profile_read(h.h)
+    cb.chase_profile_enable(h.h, False)
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(ms_local)
+    hemm_ms = allmax(prof_ms["hemm"])
+    filt_ms = allmax(prof_ms["hemm"] + prof_ms["allreduce"] - 0.0)
+    F = filter_flops(w, degrees)
+    value = F * args.steps / (ms / 1e3) / 1e12
+    per_gpu_hemm_flops = F / n_gpus                            # per filter call per GPU
+    launches_per_filter = int(np.max(degrees))
+    hemm_avg_ms = hemm_ms / (args.steps * launches_per_filter)
+    hemm_achieved = per_gpu_hemm_flops / launches_per_filter / (hemm_avg_ms / 1e3) / 1e12
+    gpu_launches = int(sum(prof_n[k] for k in ("hemm", "gram", "potrf", "trsm", "other")))
+
+    # ---- end-to-end through the public API with host buffers (V in from pinned host, V out)
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            V_t.copy_(V0_host, non_blocking=True)
+            step()
+            out_host.copy_(V_t, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        e2e_ms = allmax(e0.elapsed_time(e1))
+        nbytes = V0_host.numel() * V0_host.element_size()
+        e2e = {"value": F * args.steps / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": int(nbytes),
+               "d2h_bytes_per_step": int(nbytes),
+               "note": "A_local resident (set once, as the paper distributes H once); V copied in and out every step"}
+
+    # ---- CPU oracle baseline on a bounded sample of the same workload (rank 0, N=1)
+    cpu = None
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
+        torch.set_num_threads(cores())
+        A_host = A_t.cpu().numpy().T                   # same bits the GPU used
+        t, fl = oracle_sample(A_host, np.asfortranarray(V0_rows), degrees, b, args.cpu_cols)
+        cpu = {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": cores(), "kind": "oracle",
+               "sample": f"oracle.chebyshev_filter on {args.cpu_cols} of {n} columns (degree "
+                         f"{int(degrees[0])}), full {N}x{N} A copied from the device, {t:.1f} s"}
+        del A_host
+
+    # ---- traffic from the committed ncu --set full capture of the HEMM kernel (if present)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "hemm_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("workload") == w["name"]:
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": n_gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w["desc"], "grid": f"{p}x{q}", "N": N, "n": n,
+                       "sum_degrees": int(np.sum(degrees)),
+                       "step": "chase_filter + chase_cholqr (Alg.4 variant from Alg.5 estimate)",
+                       "l2": "no flush needed: A_local is larger than the 126 MB L2 "
+                             f"({16 * n_r * n_c / 1e9:.1f} GB per GPU)",
+                       "parallelism": f"2D block grid {p}x{q}, NCCL allreduce"},
+            "pct_of_fp64_peak_per_gpu": 100.0 * value / n_gpus / FP64_PEAK_TFLOPS,
+            "filter_only_tflops": F * args.steps / (filt_ms / 1e3) / 1e12,
+            "qr": {"variant": qr_info["variant"], "passes": qr_info["passes"],
+                   "ms_per_step": (ms - filt_ms) / args.steps, "cond_est": est,
+                   "tflops": qr_flops(w, n, qr_info["passes"]) / n_gpus * args.steps /
+                             max(1e-9, (ms - filt_ms) / 1e3) / 1e12},
+            "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (HEMM step)" if w["complex_"] else "dgemm_kernel",
+                         "achieved": hemm_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": hemm_achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01/fp64_peak.log); "
+                                        "MEASURED_PEAKS.json has no FP64 entry",
+                         "per_launch_flops": per_gpu_hemm_flops / launches_per_filter,
+                         "avg_launch_ms": hemm_avg_ms},
+            "profile_ms_per_step": {k: v / args.steps for k, v in prof_ms.items()},
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
