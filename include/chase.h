@@ -202,11 +202,11 @@ double chase_shift_value(int64_t m, int64_t n, double norm);
 /* ---------------------------------------------------------------------------------------
  * Measurement support (bench.py): when enabled, CUDA events bracket every launch on the
  * handle's stream; chase_profile_read synchronises, returns per-category device time (ms)
- * and launch counts since the last read, and resets.  Categories:
- *   0 HEMM (filter steps)  1 AllReduce  2 Gram  3 POTRF  4 TRSM  5 other kernels
- * ms and launches are host arrays of 6 entries. */
+ * and kernel-launch counts since the last read, and resets.  Categories (arrays of 8):
+ *   0 HEMM odd steps (A^H C -> B)   1 HEMM even steps (A B -> C)   2 AllReduce (NCCL calls)
+ *   3 Gram   4 POTRF   5 TRSM   6 other kernels   7 reserved (0) */
 chase_status_t chase_profile_enable(chase_handle_t h, int enable);
-chase_status_t chase_profile_read(chase_handle_t h, double ms[6], int64_t launches[6]);
+chase_status_t chase_profile_read(chase_handle_t h, double ms[8], int64_t launches[8]);
 
 chase_status_t chase_destroy(chase_handle_t h);
 const char* chase_status_string(chase_status_t s);

@@ -25,7 +25,7 @@ CHASE_QR_CHOL1, CHASE_QR_CHOL2, CHASE_QR_SHIFTED = 1, 2, 3
 STATUS = {0: "CHASE_OK", 1: "CHASE_EINVAL", 2: "CHASE_EDEGREE", 3: "CHASE_EBOUNDS",
           4: "CHASE_ECHOL", 5: "CHASE_ECUDA", 6: "CHASE_ENCCL", 7: "CHASE_ENOMEM",
           8: "CHASE_ESTATE"}
-PROFILE_CATEGORIES = ("hemm", "allreduce", "gram", "potrf", "trsm", "other")
+PROFILE_CATEGORIES = ("hemm_odd", "hemm_even", "allreduce", "gram", "potrf", "trsm", "other", "reserved")
 
 # every symbol include/chase.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -245,11 +245,14 @@ def chase_profile_enable(h, enable: bool = True):
 
 
 def chase_profile_read(h):
-    ms = (ctypes.c_double * 6)()
-    ln = (ctypes.c_int64 * 6)()
+    ms = (ctypes.c_double * 8)()
+    ln = (ctypes.c_int64 * 8)()
     _check(load().chase_profile_read(h, ms, ln), "chase_profile_read")
-    return ({k: ms[i] for i, k in enumerate(PROFILE_CATEGORIES)},
-            {k: ln[i] for i, k in enumerate(PROFILE_CATEGORIES)})
+    ms_d = {k: ms[i] for i, k in enumerate(PROFILE_CATEGORIES)}
+    ln_d = {k: ln[i] for i, k in enumerate(PROFILE_CATEGORIES)}
+    ms_d["hemm"] = ms_d["hemm_odd"] + ms_d["hemm_even"]
+    ln_d["hemm"] = ln_d["hemm_odd"] + ln_d["hemm_even"]
+    return ms_d, ln_d
 
 
 def chase_destroy(h):

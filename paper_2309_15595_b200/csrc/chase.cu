@@ -92,7 +92,7 @@ static void block_part(int64_t N, int P, int k, int64_t* size, int64_t* start) {
 }
 
 // ==================================================================== handle
-enum { CAT_HEMM = 0, CAT_ALLREDUCE, CAT_GRAM, CAT_POTRF, CAT_TRSM, CAT_OTHER, CAT_N };
+enum { CAT_HEMM_ODD = 0, CAT_HEMM_EVEN, CAT_ALLREDUCE, CAT_GRAM, CAT_POTRF, CAT_TRSM, CAT_OTHER, CAT_N };
 
 struct chase_handle_s {
   chase_dtype_t dt;
@@ -179,6 +179,7 @@ static void ws_layout(const chase_handle_s* h, size_t* b_off, size_t* g_off, siz
 
 // ==================================================================== GEMM launchers
 static bool g_attr_done[2][2] = {{false, false}, {false, false}};
+static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a) {
@@ -240,6 +241,7 @@ struct GemmReq {
   double alpha, beta, c;
   int use_beta, band_lo, band_hi, band_shift, upper_only;
   const int* abort_flag;
+  int a3d;                   // NoTrans: tA is the 3D single-box view (a_d0 multiple of a piece)
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
@@ -252,6 +254,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
     a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
     a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+    a.a3d = r.a3d;
     return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
   }
   DGemmArgs a;
@@ -262,13 +265,46 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
   a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
   a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+  a.a3d = r.a3d;
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
 }
 
 // Tensor maps for the three roles a matrix plays in the GEMM (box shapes of zgemm / dgemm).
 enum MapRole { ROLE_A_NOTRANS, ROLE_A_TRANS, ROLE_X };
+// 3D view of a column-major matrix for the NoTrans A tile: dims {one 128-byte row piece,
+// columns, row pieces} so one TMA box fills the whole BM x BK tile.  Only valid when every
+// column has room for whole 128-byte pieces (ld >= rows rounded up to a piece), since TMA
+// bounds-checks per dimension and the last piece may run past the column's rows.
+static chase_status_t make_map_3d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
+                                  int64_t ld, int esize, int box_k, int box_pieces) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return CHASE_ECUDA;
+  const int piece = 128 / esize;                       // elements per 128-byte row piece
+  cuuint64_t dims[3] = {16, (cuuint64_t)cols, (cuuint64_t)((rows + piece - 1) / piece)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * esize), 128};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_k, (cuuint32_t)box_pieces};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? CHASE_OK : CHASE_ECUDA;
+}
+
 static chase_status_t make_role_map(const chase_handle_s* h, CUtensorMap* m, const void* base,
-                                    int64_t rows, int64_t cols, int64_t ld, MapRole role) {
+                                    int64_t rows, int64_t cols, int64_t ld, MapRole role,
+                                    int* a3d = nullptr) {
+  const int es = (int)esize_of(h->dt);
+  if (a3d) *a3d = 0;
+  if (role == ROLE_A_NOTRANS && a3d && !g_disable_a3d) {
+    const int piece = 128 / es;
+    const int64_t rows_up = (rows + piece - 1) / piece * piece;
+    if (ld >= rows_up &&
+        make_map_3d(m, base, rows, cols, ld, es, es == 16 ? 8 : DG_BK,
+                    es == 16 ? ZG_BM / 8 : DG_BM / 16) == CHASE_OK) {
+      *a3d = 1;
+      return CHASE_OK;
+    }
+  }
   if (h->dt == CHASE_C128) {
     const int bc = role == ROLE_A_NOTRANS ? 8 : role == ROLE_A_TRANS ? ZG_BM : ZG_BN;
     return make_map(m, base, rows, cols, ld, 16, 8, bc);
@@ -518,7 +554,8 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
 
   const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
   CUtensorMap tA_nt, tA_t, tC, tB;
-  STATUS_TRY(make_role_map(h, &tA_nt, A_local, n_r, n_c, lda, ROLE_A_NOTRANS));
+  int a3d = 0;
+  STATUS_TRY(make_role_map(h, &tA_nt, A_local, n_r, n_c, lda, ROLE_A_NOTRANS, &a3d));
   STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
   STATUS_TRY(make_role_map(h, &tC, V, n_r, ncols, ldv, ROLE_X));
   STATUS_TRY(make_role_map(h, &tB, h->Bws, n_c, ncols, ldb, ROLE_X));
@@ -533,6 +570,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     g.c = c;
     g.upper_only = 0;
     g.abort_flag = nullptr;
+    g.a3d = 0;
     g.x_k0 = 0;
     g.x_n0 = r.off;
     g.a_d0 = 0;
@@ -557,6 +595,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       // C_i = alpha (A_ij B_j - c band(B_j)) + [j == 0] beta C_i
       g.conj = false;
       g.tA = &tA_nt;
+      g.a3d = a3d;
       g.tX = &tB;
       g.M = (int)n_r;
       g.K = (int)n_c;
@@ -570,7 +609,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.use_beta = (h->mycol == 0) ? 1 : 0;
     }
     {
-      ProfScope ps(h, CAT_HEMM, 1);
+      ProfScope ps(h, s % 2 == 1 ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
       STATUS_TRY(run_gemm(h, g));
     }
     if (s % 2 == 1 && h->p > 1) STATUS_TRY(allreduce(h, g.out, (size_t)ldb * r.k, h->ccomm));
@@ -609,6 +648,7 @@ void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n
 
 struct QrMaps {
   CUtensorMap vA_t, vA_nt, vX, gA_t, gX;
+  int v_a3d = 0;
 };
 
 // One Gram/POTRF/TRSM round; returns CHASE_ECHOL with *info set when POTRF fails (V untouched).
@@ -688,7 +728,7 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
       if (rest > 0) {
         // V[:, kb+nb:] -= V[:, kb:kb+nb] R[kb:kb+nb, kb+nb:]
         GemmReq g{};
-        g.conj = false; g.tA = &mp.vA_nt; g.tX = &mp.gX;
+        g.conj = false; g.tA = &mp.vA_nt; g.tX = &mp.gX; g.a3d = mp.v_a3d;
         g.M = (int)n_r; g.N = rest; g.K = nb;
         g.a_d0 = 0; g.a_d1 = kb; g.x_k0 = kb; g.x_n0 = kb + nb;
         g.out = Vc + (size_t)(kb + nb) * ldv * es; g.ldo = ldv;
@@ -726,7 +766,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   const int n = (int)ncols;
   QrMaps mp;
   STATUS_TRY(make_role_map(h, &mp.vA_t, V, h->n_r, n, ldv, ROLE_A_TRANS));
-  STATUS_TRY(make_role_map(h, &mp.vA_nt, V, h->n_r, n, ldv, ROLE_A_NOTRANS));
+  STATUS_TRY(make_role_map(h, &mp.vA_nt, V, h->n_r, n, ldv, ROLE_A_NOTRANS, &mp.v_a3d));
   STATUS_TRY(make_role_map(h, &mp.vX, V, h->n_r, n, ldv, ROLE_X));
   STATUS_TRY(make_role_map(h, &mp.gA_t, h->Gws, n, n, pad_ld(n), ROLE_A_TRANS));
   STATUS_TRY(make_role_map(h, &mp.gX, h->Gws, n, n, pad_ld(n), ROLE_X));
@@ -788,10 +828,13 @@ chase_status_t chase_profile_enable(chase_handle_t h, int enable) {
   return CHASE_OK;
 }
 
-chase_status_t chase_profile_read(chase_handle_t h, double ms[6], int64_t launches[6]) {
+chase_status_t chase_profile_read(chase_handle_t h, double ms[8], int64_t launches[8]) {
   if (!h || !ms || !launches) return CHASE_EINVAL;
   CUDA_TRY(cudaStreamSynchronize(h->stream));
-  for (int i = 0; i < CAT_N; ++i) ms[i] = 0.0;
+  for (int i = 0; i < 8; ++i) {
+    ms[i] = 0.0;
+    launches[i] = 0;
+  }
   for (auto& ev : h->evs) {
     float t = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&t, ev.a, ev.b));

@@ -54,6 +54,16 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 3D tile load (used for the NoTrans A tile: dims {128-byte row piece, k, 128-byte row index})
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ------------------------------------------------------------------ DMMA
 // D(16x8) += A(16x4, row) * B(4x8, col), f64.  Fragment layout (g = lane/4, t = lane%4):
 //   a0 = A[g][t], a1 = A[g+8][t];  b0 = B[t][g];

@@ -40,6 +40,7 @@ struct DGemmArgs {
   int band_shift;
   int upper_only;
   const int* abort_flag;
+  int a3d;                 // NoTrans only: tmA is the 3D view {16 doubles, k, m/16} -> 1 TMA/stage
 };
 
 __device__ __forceinline__ int dg_kperm(int t, int h) {
@@ -80,9 +81,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     if (TRANS) {
       tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);     // box 16 k x 128 m
     } else {
+      if (g.a3d) {
+        tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 16, &full[s]);
+      } else {
 #pragma unroll
-      for (int b = 0; b < DG_BM / 16; ++b)                      // box 16 m x 16 k
-        tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+        for (int b = 0; b < DG_BM / 16; ++b)                    // box 16 m x 16 k
+          tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+      }
     }
     tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);       // box 16 k x 128 n
   };

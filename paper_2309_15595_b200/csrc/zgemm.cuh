@@ -48,6 +48,7 @@ struct ZGemmArgs {
   int band_shift;
   int upper_only;          // skip CTAs whose tile lies strictly below the diagonal (m > n)
   const int* abort_flag;   // non-null: skip the whole GEMM when *abort_flag != 0 (POTRF info)
+  int a3d;                 // NoTrans only: tmA is the 3D view {8 complex, k, m/8} -> 1 TMA/stage
 };
 
 template <bool CONJ>
@@ -86,9 +87,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       tma_load_2d(sa, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
     } else {
       // A rows (m) contiguous: 16 boxes of 8 m x 8 k, box b holds rows [8b, 8b+8), row = k
+      if (g.a3d) {
+        tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 8, &full[s]);
+      } else {
 #pragma unroll
-      for (int b = 0; b < ZG_BM / 8; ++b)
-        tma_load_2d(sa + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+        for (int b = 0; b < ZG_BM / 8; ++b)
+          tma_load_2d(sa + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+      }
     }
     tma_load_2d(sx, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
   };
