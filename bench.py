@@ -8,7 +8,7 @@ synthetic workload, through the C-ABI (libchase.so).
 
 Workloads (BASELINE.json configs, synthetic, seeded):
     N=1  C2: N=30000 complex Hermitian, Uniform spectrum, nev=2250 nex=750, degree 20, 1x1
-    N=2  weak-scaling point of C2 (paper Fig.3a recipe, N = 30000 sqrt(P)): N=42426, n=3000, 2x1
+    N=2  weak-scaling point of C2 (paper Fig.3a recipe, N ~ 30000 sqrt(P)): N=42432, n=3000, 2x1
     N=4  N=60000, n=3000, 2x2
     N=8  C4: N=120000 complex Uniform, nev=1200 nex=400, degree 20, 2x4 (north-star target)
 Metric (BASELINE.json): Chebyshev filter FP64 TFLOP/s (max over ranks): algorithmic filter
@@ -44,7 +44,7 @@ def workload(n_gpus: int, name: str):
     if name == "auto":
         name = {1: "C2", 8: "C4"}.get(n_gpus, "W")
     if name == "W":   # weak-scaling point of C2 (N grows with sqrt(#GPUs))
-        N = int(round(30000 * math.sqrt(n_gpus)))
+        N = 16 * int(round(30000 * math.sqrt(n_gpus) / 16))    # multiple of 16: 3D TMA path
         return dict(name=f"W{n_gpus}", N=N, nev=2250, nex=750, complex_=True, spectrum="uniform",
                     seed=2, degree=20,
                     desc=f"C2 weak-scaling point: N={N} complex Hermitian Uniform, nev=2250 nex=750, "
@@ -248,11 +248,8 @@ def main():
 
     uid = None
     if world > 1:
-        t = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(cb.chase_get_unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().numpy().tobytes())
+        from paper_2309_15595_b200 import dist as cdist
+        uid = cdist.share_unique_id(cb.chase_get_unique_id)
     stream = torch.cuda.current_stream(dev)
     h = cb.Chase(dtype, N, n, p, q, myrow, mycol, uid, local, stream)
     n_r, n_c, r0, c0 = h.n_r, h.n_c, h.r0, h.c0

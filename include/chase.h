@@ -70,13 +70,18 @@ typedef struct {
  * communicator) and 1 for an even step (result in C-layout, AllReduce over the row
  * communicator), elems = complex/real elements in this rank's AllReduce message
  * (n_c*k for odd, n_r*k for even); the AllReduce is skipped when that communicator has a
- * single member (p == 1 for odd steps, q == 1 for even steps). */
+ * single member (p == 1 for odd steps, q == 1 for even steps).
+ * use_beta = 1 when this rank adds beta_s * V_{s-2} before the AllReduce (the first rank of
+ * the reducing communicator, never at s = 1; reading #7); [band_lo, band_hi) = local output
+ * rows to which this rank applies the -c I shift (its share of the diagonal; reading #6). */
 typedef struct {
   int32_t k;
   int32_t off;
   int32_t comm;
-  int32_t reserved;
+  int32_t use_beta;
   int64_t elems;
+  int32_t band_lo;
+  int32_t band_hi;
 } chase_step_record_t;
 
 typedef struct chase_handle_s* chase_handle_t;

@@ -55,7 +55,8 @@ class chase_stats_t(ctypes.Structure):
 
 class chase_step_record_t(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("off", ctypes.c_int32), ("comm", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("elems", ctypes.c_int64)]
+                ("use_beta", ctypes.c_int32), ("elems", ctypes.c_int64),
+                ("band_lo", ctypes.c_int32), ("band_hi", ctypes.c_int32)]
 
 
 _lib = None
@@ -190,19 +191,26 @@ def chase_filter(h, A_local, V, degrees, c: float, e: float, bounds, ncols: int 
     return {"matvecs": st.matvecs, "steps": st.steps}
 
 
-def _records(n, rec):
-    return [(rec[i].k, rec[i].off, "col" if rec[i].comm == 0 else "row", rec[i].elems) for i in range(n)]
+def _records(n, rec, full: bool = False):
+    """(k, off, comm, elems) per step, the oracle's record schema; full=True appends
+    (use_beta, band_lo, band_hi)."""
+    out = []
+    for i in range(n):
+        r = rec[i]
+        t = (r.k, r.off, "col" if r.comm == 0 else "row", r.elems)
+        out.append(t + (r.use_beta, r.band_lo, r.band_hi) if full else t)
+    return out
 
 
-def chase_filter_record(h):
+def chase_filter_record(h, full: bool = False):
     ns, mv = ctypes.c_int32(), ctypes.c_int64()
     _check(load().chase_filter_record(h, 0, None, ctypes.byref(ns), ctypes.byref(mv)), "chase_filter_record")
     rec = (chase_step_record_t * max(1, ns.value))()
     _check(load().chase_filter_record(h, ns.value, rec, ctypes.byref(ns), ctypes.byref(mv)), "chase_filter_record")
-    return _records(ns.value, rec), mv.value
+    return _records(ns.value, rec, full), mv.value
 
 
-def chase_filter_schedule(N: int, p: int, q: int, myrow: int, mycol: int, degrees):
+def chase_filter_schedule(N: int, p: int, q: int, myrow: int, mycol: int, degrees, full: bool = False):
     arr, dp = _i32_array(degrees)
     ns, mv = ctypes.c_int32(), ctypes.c_int64()
     _check(load().chase_filter_schedule(N, p, q, myrow, mycol, arr.shape[0], dp, 0, None,
@@ -210,7 +218,7 @@ def chase_filter_schedule(N: int, p: int, q: int, myrow: int, mycol: int, degree
     rec = (chase_step_record_t * max(1, ns.value))()
     _check(load().chase_filter_schedule(N, p, q, myrow, mycol, arr.shape[0], dp, ns.value, rec,
                                         ctypes.byref(ns), ctypes.byref(mv)), "chase_filter_schedule")
-    return _records(ns.value, rec), mv.value
+    return _records(ns.value, rec, full), mv.value
 
 
 def chase_cholqr(h, V, cond_est: float, ncols: int | None = None, raise_on_error: bool = True):

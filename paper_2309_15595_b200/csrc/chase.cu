@@ -345,7 +345,13 @@ static chase_status_t validate_degrees(int64_t ncols, const int32_t* degrees) {
   return CHASE_OK;
 }
 
-static void build_schedule(int64_t n_r, int64_t n_c, int64_t ncols, const int32_t* degrees,
+// The per-step schedule of rank (myrow, mycol): active width, offset, communicator, message
+// size, and the rank's share of the -cI shift (band) and of the beta term (use_beta).
+struct Geom {
+  int64_t n_r, n_c, r0, c0;
+  int myrow, mycol;
+};
+static void build_schedule(const Geom& gm, int64_t ncols, const int32_t* degrees,
                            std::vector<chase_step_record_t>* rec, int64_t* matvecs) {
   const int32_t D = degrees[ncols - 1];
   rec->assign(D, chase_step_record_t{});
@@ -355,11 +361,20 @@ static void build_schedule(int64_t n_r, int64_t n_c, int64_t ncols, const int32_
   for (int32_t s = 1; s <= D; ++s) {
     while (first < ncols && degrees[first] < s) ++first;
     chase_step_record_t& r = (*rec)[s - 1];
+    const bool odd = (s % 2 == 1);
     r.k = (int32_t)(ncols - first);
     r.off = (int32_t)first;
-    r.comm = (s % 2 == 1) ? 0 : 1;
-    r.reserved = 0;
-    r.elems = (int64_t)r.k * (s % 2 == 1 ? n_c : n_r);
+    r.comm = odd ? 0 : 1;
+    r.elems = (int64_t)r.k * (odd ? gm.n_c : gm.n_r);
+    if (odd) {   // output rows = B_j rows (global c0 + row); diagonal rows also in [r0, r0+n_r)
+      r.band_lo = (int32_t)std::max<int64_t>(0, gm.r0 - gm.c0);
+      r.band_hi = (int32_t)std::max<int64_t>(r.band_lo, std::min<int64_t>(gm.n_c, gm.r0 + gm.n_r - gm.c0));
+      r.use_beta = (gm.myrow == 0 && s > 1) ? 1 : 0;
+    } else {     // output rows = C_i rows (global r0 + row); diagonal rows also in [c0, c0+n_c)
+      r.band_lo = (int32_t)std::max<int64_t>(0, gm.c0 - gm.r0);
+      r.band_hi = (int32_t)std::max<int64_t>(r.band_lo, std::min<int64_t>(gm.n_r, gm.c0 + gm.n_c - gm.r0));
+      r.use_beta = (gm.mycol == 0) ? 1 : 0;
+    }
   }
   *matvecs = mv;
 }
@@ -493,7 +508,7 @@ chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int myc
   STATUS_TRY(validate_degrees(ncols, degrees));
   std::vector<chase_step_record_t> r;
   int64_t mv;
-  build_schedule(n_r, n_c, ncols, degrees, &r, &mv);
+  build_schedule(Geom{n_r, n_c, r0, c0, myrow, mycol}, ncols, degrees, &r, &mv);
   *nsteps = (int32_t)r.size();
   if (matvecs) *matvecs = mv;
   if (rec) {
@@ -535,7 +550,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
 
   std::vector<chase_step_record_t> rec;
   int64_t mv;
-  build_schedule(h->n_r, h->n_c, ncols, degrees, &rec, &mv);
+  build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol}, ncols, degrees, &rec, &mv);
   const int D = (int)rec.size();
 
   // recurrence scalars: alpha_1 = sigma_1/e, beta_1 = 0; alpha_s = 2 sigma_s/e,
@@ -587,10 +602,10 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.ldo = ldb;
       g.xin = Vc + (size_t)r.off * ldv * es;
       g.ldx = ldv;
-      g.band_lo = (int)std::max<int64_t>(0, h->r0 - h->c0);
-      g.band_hi = (int)std::min<int64_t>(n_c, h->r0 + n_r - h->c0);
-      g.band_shift = (int)(h->c0 - h->r0);
-      g.use_beta = (h->myrow == 0 && s > 1) ? 1 : 0;
+      g.band_lo = r.band_lo;
+      g.band_hi = r.band_hi;
+      g.band_shift = (int)(h->c0 - h->r0);   // input C row = output B row + c0 - r0
+      g.use_beta = r.use_beta;
     } else {
       // C_i = alpha (A_ij B_j - c band(B_j)) + [j == 0] beta C_i
       g.conj = false;
@@ -603,10 +618,10 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.ldo = ldv;
       g.xin = Bc + (size_t)r.off * ldb * es;
       g.ldx = ldb;
-      g.band_lo = (int)std::max<int64_t>(0, h->c0 - h->r0);
-      g.band_hi = (int)std::min<int64_t>(n_r, h->c0 + n_c - h->r0);
-      g.band_shift = (int)(h->r0 - h->c0);
-      g.use_beta = (h->mycol == 0) ? 1 : 0;
+      g.band_lo = r.band_lo;
+      g.band_hi = r.band_hi;
+      g.band_shift = (int)(h->r0 - h->c0);   // input B row = output C row + r0 - c0
+      g.use_beta = r.use_beta;
     }
     {
       ProfScope ps(h, s % 2 == 1 ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);

@@ -1,0 +1,72 @@
+"""Multi-GPU parity (torchrun, one rank per GPU, NCCL over NVLink): the 2D-distributed filter
+and the 1D-CAQR over the column communicator match the global oracle; replicas across the
+row communicator are bitwise identical; bookkeeping equals the oracle's per-rank record.
+Skipped when fewer than 2 GPUs are visible."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import chase_inputs as ci
+import oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+GRIDS = [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)]
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("grid", GRIDS)
+def test_grid_matches_oracle(tmp_path, grid, complex_):
+    p, q = grid
+    if ngpus() < p * q:
+        pytest.skip(f"needs {p * q} GPUs")
+    N = 301
+    out = str(tmp_path / "res.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p * q}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N), "c" if complex_ else "r", out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = np.load(out)
+    degs = sorted([2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20] * 3)
+    n = len(degs)
+    lam = ci.uniform_spectrum(N)
+    A = ci.dense_from_spectrum(lam, 77, complex_)
+    V0 = ci.gaussian_block(N, n, 78, complex_)
+    b = ci.bounds_from_spectrum(lam, n)
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    V = res["V"]
+    err = np.max(np.linalg.norm(V - ref, axis=0) / np.linalg.norm(ref, axis=0))
+    assert err <= 1e-10
+    assert float(res["replica"]) == 0.0                       # identical bits on all replicas
+    assert np.all(res["mv"] == sum(degs))
+    for (i, j, nr), recs in zip(res["ranks"], res["recs"]):
+        n_r, n_c, _, _ = ci.block_dims(N, p, q, int(i), int(j))
+        orec, _ = oracle.filter_record(degs, n_r, n_c)
+        assert recs == str(orec)
+    qref = oracle.caqr(ref, float(res["est"]))
+    assert np.all(res["status"] == 0)
+    assert np.all(res["variants"] == qref["variant"]) and np.all(res["passes"] == qref["passes"])
+    Q = res["Q"]
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(n)) <= 1e-12
+    kappa = np.linalg.cond(ref)
+    assert np.linalg.norm(Q - qref["Q"]) / np.sqrt(n) <= 100 * kappa * 2.0 ** -53 + 1e-13
