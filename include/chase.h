@@ -121,8 +121,9 @@ chase_status_t chase_block_dims(int64_t N, int p, int q, int i, int j, int64_t* 
                                 int64_t* n_c, int64_t* r0, int64_t* c0);
 
 /* Bytes of device workspace the handle needs: the B-layout block n_c x n_max, the
- * n_max x n_max Gram matrix (Alg.3 l.3), and small scalars.  Memory model Eq.(2), P:216-223,
- * minus the C2/B2/A buffers of the Rayleigh-Ritz step, which are out of scope. */
+ * n_max x n_max Gram matrix (Alg.3 l.3), an n_r x n_max TRSM output block, the inverted
+ * 64 x 64 diagonal blocks of R, and small scalars -- the same order as the memory model
+ * Eq.(2), P:216-223 (N^2/(pq) is the caller's A_local). */
 chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes);
 
 /* Hand the handle `bytes` of caller-owned device memory (>= chase_workspace_size, 256-byte

@@ -1,10 +1,11 @@
 // qr_kernels.cuh -- the latency-bound pieces of 1D-CholeskyQR (Alg.3; Alg.4 l.5-7,
-// P:294-297) for complex double.  The flop-heavy pieces (Gram X^H X, the trailing HERK update
-// of the blocked POTRF and the TRSM right-looking updates) run on the tensor-core zgemm.
+// P:294-297), templated on double (real symmetric) / double2 (complex Hermitian).  The
+// flop-heavy pieces (Gram X^H X, the trailing HERK update of the blocked POTRF, the TRSM
+// diagonal-block products and right-looking updates) run on the tensor-core GEMMs.
 //
 //   potrf_diag_kernel    unblocked upper Cholesky of one nb x nb diagonal block, in smem
 //   potrf_panel_kernel   R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:]   (forward substitution)
-//   trsm_diag_kernel     X[:, kb:kb+nb] = X[:, kb:kb+nb] R_kk^{-1}  (one thread per row)
+//   trtri_diag_kernel    inverses of the 64 x 64 diagonal blocks of R (blocked TRSM)
 //   shift_kernel         norm = Re tr(G) (= ||X||_F^2, reading #12); s = 11(mn+n(n+1)) u norm;
 //                        G += s I
 // A POTRF failure (radicand <= 0 or NaN) writes the 1-based global pivot into *info once;
@@ -106,35 +107,39 @@ __global__ void __launch_bounds__(PANEL_THREADS)
   }
 }
 
-// X[:, kb:kb+nb] <- X[:, kb:kb+nb] R_kk^{-1}, R_kk = upper block of G.  One thread per row:
-//   y_l = (x_l - sum_{k<l} y_k R[k][l]) / R[l][l].
-constexpr int TRSM_THREADS = 128;
+// Inverses of the diagonal blocks of the upper-triangular R (blocked TRSM with inverted
+// diagonal blocks): CTA b inverts R[kb:kb+nb, kb:kb+nb], kb = 64 b, into Rinv[0:64, kb:kb+64]
+// (column-major, ld 64, zeros below the diagonal and in the padding of a short last block).
+// Thread j solves R_kk x = e_j by back substitution:
+//   x_j = 1 / R_jj,  x_i = -(sum_{l=i+1..j} R_il x_l) / R_ii   (i = j-1 .. 0).
+constexpr int TRTRI_NB = 64;
 template <typename T>
-constexpr int trsm_smem() { return (QR_NB * QR_NB + QR_NB * TRSM_THREADS) * (int)sizeof(T); }
+constexpr int trtri_smem() { return 2 * TRTRI_NB * TRTRI_NB * (int)sizeof(T); }
 template <typename T>
-__global__ void __launch_bounds__(TRSM_THREADS)
-    trsm_diag_kernel(T* X, long long ldx, int m, const T* G, long long ld, int kb, int nb) {
+__global__ void __launch_bounds__(TRTRI_NB)
+    trtri_diag_kernel(const T* G, long long ld, int n, T* Rinv) {
   extern __shared__ __align__(16) unsigned char qr_dyn[];
-  T (*R)[QR_NB] = reinterpret_cast<T (*)[QR_NB]>(qr_dyn);
-  T (*Y)[TRSM_THREADS] = reinterpret_cast<T (*)[TRSM_THREADS]>(qr_dyn + QR_NB * QR_NB * sizeof(T));
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < nb * nb; idx += TRSM_THREADS) {
-    const int a = idx % nb, b = idx / nb;
-    R[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
+  T (*R)[TRTRI_NB] = reinterpret_cast<T (*)[TRTRI_NB]>(qr_dyn);                 // R[i][l]
+  T (*X)[TRTRI_NB] = reinterpret_cast<T (*)[TRTRI_NB]>(qr_dyn + TRTRI_NB * TRTRI_NB * sizeof(T));
+  const int kb = blockIdx.x * TRTRI_NB;
+  const int nb = min(TRTRI_NB, n - kb);
+  const int j = threadIdx.x;
+  for (int idx = j; idx < TRTRI_NB * TRTRI_NB; idx += TRTRI_NB) {
+    const int a = idx % TRTRI_NB, b = idx / TRTRI_NB;
+    R[a][b] = (a < nb && b < nb && a <= b) ? G[(long long)(kb + a) + (long long)(kb + b) * ld]
+                                           : s_real<T>(0.0);
   }
-  const long long row = (long long)blockIdx.x * TRSM_THREADS + tid;
-  const bool active = row < m;
-  if (active)
-    for (int l = 0; l < nb; ++l) Y[l][tid] = X[row + (long long)(kb + l) * ldx];
   __syncthreads();
-  if (!active) return;
-  for (int l = 0; l < nb; ++l) {
-    T acc = Y[l][tid];
-    for (int k = 0; k < l; ++k) acc = s_sub(acc, s_mul(Y[k][tid], R[k][l]));
-    acc = s_div(acc, s_re(R[l][l]));
-    Y[l][tid] = acc;
-    X[row + (long long)(kb + l) * ldx] = acc;
+  for (int i = 0; i < TRTRI_NB; ++i) X[i][j] = s_real<T>(0.0);
+  if (j < nb) {
+    X[j][j] = s_real<T>(1.0 / s_re(R[j][j]));
+    for (int i = j - 1; i >= 0; --i) {
+      T acc = s_real<T>(0.0);
+      for (int l = i + 1; l <= j; ++l) acc = s_sub(acc, s_mul(R[i][l], X[l][j]));
+      X[i][j] = s_div(acc, s_re(R[i][i]));
+    }
   }
+  for (int i = 0; i < TRTRI_NB; ++i) Rinv[(long long)i + (long long)(kb + j) * TRTRI_NB] = X[i][j];
 }
 
 // Alg.4 l.5-7 on the reduced Gram matrix: norm = sum_j Re G[j][j]; s = 11 (m n + n (n+1)) u norm;
