@@ -18,7 +18,7 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libchase.so")
+LIB_PATH = os.environ.get("CHASE_LIB") or os.path.join(_PKG, "libchase.so")   # CHASE_LIB: A/B builds
 
 CHASE_R64, CHASE_C128 = 1, 2
 CHASE_QR_CHOL1, CHASE_QR_CHOL2, CHASE_QR_SHIFTED = 1, 2, 3

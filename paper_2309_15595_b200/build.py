@@ -34,8 +34,9 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = True, out: str | None = None, defines=()) -> str:
+    lib_out = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
     cmd = [
@@ -44,7 +45,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
         *[os.path.join(CSRC, s) for s in SOURCES],
-        "-o", LIB + ".tmp",
+        *[f"-D{d}" for d in defines],
+        "-o", lib_out + ".tmp",
         "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
     ]
     if verbose:
@@ -56,10 +58,13 @@ def build(force: bool = False, verbose: bool = True) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libchase.so (see paper_2309_15595_b200/build.log)")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
-    print("built", LIB)
+    # python -m paper_2309_15595_b200.build [--force] [--out PATH -DNAME=V ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print("built", build(force="--force" in args, out=out, defines=defs))

@@ -24,12 +24,18 @@ namespace chase {
 
 constexpr int ZG_BM = 128;        // rows of out per CTA
 constexpr int ZG_BN = 64;         // columns of out per CTA
-constexpr int ZG_BK = 8;          // complex k per stage (one 128-byte swizzle row)
-constexpr int ZG_STAGES = 8;
+#ifndef ZG_KSUB
+#define ZG_KSUB 2                 // 8-wide k slabs (one 128-byte swizzle row each) per stage
+#endif
+constexpr int ZG_KS = ZG_KSUB;
+constexpr int ZG_BK = 8 * ZG_KS;  // complex k per stage
+constexpr int ZG_STAGES = 8 / ZG_KS;
 constexpr int ZG_CONSUMERS = 8;   // consumer warps (4 along M x 2 along N)
 constexpr int ZG_THREADS = ZG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
-constexpr int ZG_A_BYTES = ZG_BM * ZG_BK * 16;   // 16 KB
-constexpr int ZG_X_BYTES = ZG_BN * ZG_BK * 16;   // 8 KB
+constexpr int ZG_A_SLAB = ZG_BM * 8 * 16;       // 16 KB per 8-wide k slab
+constexpr int ZG_X_SLAB = ZG_BN * 8 * 16;       // 8 KB per 8-wide k slab
+constexpr int ZG_A_BYTES = ZG_A_SLAB * ZG_KS;
+constexpr int ZG_X_BYTES = ZG_X_SLAB * ZG_KS;
 constexpr int ZG_STAGE_BYTES = ZG_A_BYTES + ZG_X_BYTES;
 constexpr int ZG_SMEM_BYTES = ZG_STAGES * ZG_STAGE_BYTES + 1024 + 2 * ZG_STAGES * 8;
 
@@ -81,21 +87,25 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
     uint8_t* sa = smem + s * ZG_STAGE_BYTES;
     uint8_t* sx = sa + ZG_A_BYTES;
-    const int k0 = kt * ZG_BK;
-    if (CONJ) {
-      // opA[m][k] = conj(A[k][m]); A rows (k) contiguous: one 128 x 8 box, row = m
-      tma_load_2d(sa, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
-    } else {
-      // A rows (m) contiguous: 16 boxes of 8 m x 8 k, box b holds rows [8b, 8b+8), row = k
-      if (g.a3d) {
-        tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 8, &full[s]);
-      } else {
 #pragma unroll
-        for (int b = 0; b < ZG_BM / 8; ++b)
-          tma_load_2d(sa + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+    for (int u = 0; u < ZG_KS; ++u) {
+      const int k0 = kt * ZG_BK + 8 * u;
+      uint8_t* sau = sa + u * ZG_A_SLAB;
+      if (CONJ) {
+        // opA[m][k] = conj(A[k][m]); A rows (k) contiguous: one 128 x 8 box, row = m
+        tma_load_2d(sau, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
+      } else {
+        // A rows (m) contiguous: 16 boxes of 8 m x 8 k, box b holds rows [8b, 8b+8), row = k
+        if (g.a3d) {
+          tma_load_3d(sau, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 8, &full[s]);
+        } else {
+#pragma unroll
+          for (int b = 0; b < ZG_BM / 8; ++b)
+            tma_load_2d(sau + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+        }
       }
+      tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
-    tma_load_2d(sx, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -121,8 +131,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     const uint8_t* sx = sa + ZG_A_BYTES;
     const bool tail = (kt == KT - 1) && (g.K - kt * ZG_BK < ZG_BK);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = 2 * tq + h;
+    for (int hh = 0; hh < 2 * ZG_KS; ++hh) {
+      const int u = hh >> 1, h = hh & 1;
+      const int k = 2 * tq + h;                        // k inside the 8-wide slab u
+      const uint8_t* sau = sa + u * ZG_A_SLAB;
+      const uint8_t* sxu = sx + u * ZG_X_SLAB;
       double2 a[2][2], b[4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
@@ -131,14 +144,14 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           const int m = wm * 32 + mt * 16 + r * 8 + gq;  // m & 7 == gq
           const int off = CONJ ? m * 128 + ((k ^ gq) << 4)
                                : (m >> 3) * 1024 + k * 128 + ((gq ^ k) << 4);
-          a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
+          a[mt][r] = *reinterpret_cast<const double2*>(sau + off);
         }
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const int n = wn * 32 + nt * 8 + gq;
-        b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
+        b[nt] = *reinterpret_cast<const double2*>(sxu + n * 128 + ((k ^ gq) << 4));
       }
-      if (tail && kt * ZG_BK + k >= g.K) {
+      if (tail && kt * ZG_BK + 8 * u + k >= g.K) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) a[mt][0] = a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
