@@ -197,7 +197,7 @@ static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B swi
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid((a.N + ZG_BN - 1) / ZG_BN, (a.M + ZG_BM - 1) / ZG_BM);
+  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM));
   if (conj) {
     if (!g_attr_done[1][0]) {
       CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -220,7 +220,7 @@ static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorM
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid((a.N + DG_BN - 1) / DG_BN, (a.M + DG_BM - 1) / DG_BM);
+  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM));
   if (trans) {
     if (!g_attr_done[1][1]) {
       CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

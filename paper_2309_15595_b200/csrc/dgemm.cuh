@@ -19,6 +19,7 @@ constexpr int DG_BM = 128;
 constexpr int DG_BN = 128;
 constexpr int DG_BK = 16;
 constexpr int DG_STAGES = 6;
+constexpr int DG_GROUP_M = 8;      // m-tiles per raster group
 constexpr int DG_CONSUMERS = 8;   // 4 along M x 2 along N
 constexpr int DG_THREADS = DG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
 constexpr int DG_A_BYTES = DG_BM * DG_BK * 8;   // 16 KB
@@ -58,7 +59,14 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   uint64_t* empty = full + DG_STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * DG_BM, n0 = blockIdx.x * DG_BN;
+  // grouped rasterisation (1D grid): consecutive CTAs walk DG_GROUP_M m-tiles, then the next
+  // n-tile, so the CTAs resident at one time share A rows and X columns in L2
+  const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
+  const int group = blockIdx.x / (DG_GROUP_M * n_tiles);
+  const int first_m = group * DG_GROUP_M;
+  const int gm = min(DG_GROUP_M, m_tiles - first_m);
+  const int within = blockIdx.x - group * DG_GROUP_M * n_tiles;
+  const int m0 = (first_m + within % gm) * DG_BM, n0 = (within / gm) * DG_BN;
   if (g.upper_only && m0 > n0 + DG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT = (g.K + DG_BK - 1) / DG_BK;

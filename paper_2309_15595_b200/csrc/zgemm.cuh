@@ -30,6 +30,7 @@ constexpr int ZG_BN = 64;         // columns of out per CTA
 constexpr int ZG_KS = ZG_KSUB;
 constexpr int ZG_BK = 8 * ZG_KS;  // complex k per stage
 constexpr int ZG_STAGES = 8 / ZG_KS;
+constexpr int ZG_GROUP_M = 8;      // m-tiles per raster group
 constexpr int ZG_CONSUMERS = 8;   // consumer warps (4 along M x 2 along N)
 constexpr int ZG_THREADS = ZG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
 constexpr int ZG_A_SLAB = ZG_BM * 8 * 16;       // 16 KB per 8-wide k slab
@@ -68,7 +69,14 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   uint64_t* empty = full + ZG_STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * ZG_BM, n0 = blockIdx.x * ZG_BN;
+  // grouped rasterisation (1D grid): consecutive CTAs walk ZG_GROUP_M m-tiles, then the next
+  // n-tile, so the CTAs resident at one time share A rows and X columns in L2
+  const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
+  const int group = blockIdx.x / (ZG_GROUP_M * n_tiles);
+  const int first_m = group * ZG_GROUP_M;
+  const int gm = min(ZG_GROUP_M, m_tiles - first_m);
+  const int within = blockIdx.x - group * ZG_GROUP_M * n_tiles;
+  const int m0 = (first_m + within % gm) * ZG_BM, n0 = (within / gm) * ZG_BN;
   if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
