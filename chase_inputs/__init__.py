@@ -57,11 +57,18 @@ def clement_spectrum(N: int) -> np.ndarray:
 
 
 def wilkinson_spectrum(N: int) -> np.ndarray:
+    """Eigenvalues of W+_N = tridiag(1, |i - (N-1)/2|, 1), ascending.  N = 200000 (config C5)
+    is precomputed by chase_inputs/make_wilkinson.py (LAPACK dsterf on the two persymmetric
+    halves) and loaded from chase_inputs/data; other N are computed here."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", f"wilkinson_{N}.npy")
+    if os.path.exists(path):
+        return np.load(path)
     from scipy.linalg import eigvalsh_tridiagonal
 
     d = np.abs(np.arange(N, dtype=np.float64) - (N - 1) / 2.0)
     off = np.ones(N - 1, dtype=np.float64)
-    return np.sort(eigvalsh_tridiagonal(d, off, lapack_driver="stebz"))
+    return np.sort(eigvalsh_tridiagonal(d, off, lapack_driver="sterf" if N > 2000 else "stebz"))
 
 
 # ----------------------------------------------------------------------------- small dense A

@@ -70,3 +70,30 @@ def test_grid_matches_oracle(tmp_path, grid, complex_):
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(n)) <= 1e-12
     kappa = np.linalg.cond(ref)
     assert np.linalg.norm(Q - qref["Q"]) / np.sqrt(n) <= 100 * kappa * 2.0 ** -53 + 1e-13
+
+
+FULL = [("C3", (2, 1)), ("C3", (2, 2)), ("C3", (2, 4)), ("C4", (2, 2)), ("C4", (2, 4)),
+        ("C5", (2, 2)), ("C5", (2, 4))]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,grid", FULL)
+def test_full_size_grid(tmp_path, name, grid):
+    """BASELINE configurations on the 2D grid: closed-form filter check of sampled columns on every
+    rank, per-rank bookkeeping, Alg.4 variant and distributed orthogonality (tests/full_worker.py)."""
+    import json
+    p, q = grid
+    if ngpus() < p * q:
+        pytest.skip(f"needs {p * q} GPUs")
+    out = str(tmp_path / "full.json")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p * q}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "full_worker.py"), name, str(p), str(q), out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for res in json.load(open(out)):
+        print(res)
+        assert res["closed_form_col_err"] <= 1e-10, res
+        assert res["record_equal"], res
+        assert res["qr_variant"] == res["oracle_variant"], res
+        assert res["orth"] <= 1e-12, res
