@@ -30,6 +30,17 @@ def _port():
     return p
 
 
+def torchrun(nproc, script_args, timeout):
+    """Launch a torchrun job on 127.0.0.1; retry on a rendezvous port collision."""
+    for attempt in range(4):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), *script_args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        if r.returncode == 0 or "EADDRINUSE" not in (r.stdout + r.stderr):
+            return r
+    return r
+
+
 GRIDS = [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)]
 
 
@@ -41,10 +52,8 @@ def test_grid_matches_oracle(tmp_path, grid, complex_):
         pytest.skip(f"needs {p * q} GPUs")
     N = 301
     out = str(tmp_path / "res.npz")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p * q}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N), "c" if complex_ else "r", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = torchrun(p * q, [os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N),
+                         "c" if complex_ else "r", out], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = np.load(out)
     degs = sorted([2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20] * 3)
@@ -86,10 +95,7 @@ def test_full_size_grid(tmp_path, name, grid):
     if ngpus() < p * q:
         pytest.skip(f"needs {p * q} GPUs")
     out = str(tmp_path / "full.json")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p * q}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "full_worker.py"), name, str(p), str(q), out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    r = torchrun(p * q, [os.path.join(ROOT, "tests", "full_worker.py"), name, str(p), str(q), out], 1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for res in json.load(open(out)):
         print(res)
