@@ -15,15 +15,25 @@
 
 namespace chase {
 
-constexpr int DG_BM = 128;
-constexpr int DG_BN = 128;
+#ifndef DG_BM_
+#define DG_BM_ 128
+#endif
+#ifndef DG_BN_
+#define DG_BN_ 128
+#endif
+constexpr int DG_BM = DG_BM_;
+constexpr int DG_BN = DG_BN_;
 constexpr int DG_BK = 16;
-constexpr int DG_STAGES = 6;
+constexpr int DG_WM = DG_BM / 4;                 // warp tile rows (4 warps along M)
+constexpr int DG_WN = DG_BN / 2;                 // warp tile cols (2 warps along N)
+constexpr int DG_MT = DG_WM / 16;                // m16 tiles per warp
+constexpr int DG_NT = DG_WN / 8;                 // n8 tiles per warp
+constexpr int DG_STAGES = 196608 / ((DG_BM + DG_BN) * DG_BK * 8);
 constexpr int DG_GROUP_M = 8;      // m-tiles per raster group
 constexpr int DG_CONSUMERS = 8;   // 4 along M x 2 along N
 constexpr int DG_THREADS = DG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
-constexpr int DG_A_BYTES = DG_BM * DG_BK * 8;   // 16 KB
-constexpr int DG_X_BYTES = DG_BN * DG_BK * 8;   // 16 KB
+constexpr int DG_A_BYTES = DG_BM * DG_BK * 8;
+constexpr int DG_X_BYTES = DG_BN * DG_BK * 8;
 constexpr int DG_STAGE_BYTES = DG_A_BYTES + DG_X_BYTES;
 constexpr int DG_SMEM_BYTES = DG_STAGES * DG_STAGE_BYTES + 1024 + 2 * DG_STAGES * 8;
 
@@ -53,8 +63,9 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const DGemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment for the 128B swizzle, derived from the __shared__ array so every
+  // fragment load stays an LDS (a pointer rebuilt from an integer becomes a generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DG_STAGES * DG_STAGE_BYTES);
   uint64_t* empty = full + DG_STAGES;
 
@@ -107,52 +118,68 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
 
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  double acc[2][8][4];
+  double acc[DG_MT][DG_NT][4];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < DG_MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < DG_NT; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
+  // fragments double-buffered across sub-steps and k-tiles (see zgemm.cuh)
+  constexpr int SUBS = DG_BK / 4;
+  struct Frag {
+    double a[DG_MT][2], b[DG_NT];
+  };
+  auto load = [&](Frag& f, int kt, int h) {
+    const int k = dg_kperm(tq, h);
+    const uint8_t* sa = smem + (kt % DG_STAGES) * DG_STAGE_BYTES;
+    const uint8_t* sx = sa + DG_A_BYTES;
+#pragma unroll
+    for (int mt = 0; mt < DG_MT; ++mt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int m = wm * DG_WM + mt * 16 + r * 8 + gq;
+        const int off = TRANS ? m * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3))
+                              : (m >> 4) * 2048 + k * 128 +
+                                    (((((m & 15) >> 1) ^ (k & 7)) << 4) | ((m & 1) << 3));
+        f.a[mt][r] = *reinterpret_cast<const double*>(sa + off);
+      }
+#pragma unroll
+    for (int nt = 0; nt < DG_NT; ++nt) {
+      const int n = wn * DG_WN + nt * 8 + gq;
+      f.b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
+    }
+    if (kt * DG_BK + k >= g.K) {
+#pragma unroll
+      for (int mt = 0; mt < DG_MT; ++mt) f.a[mt][0] = f.a[mt][1] = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < DG_NT; ++nt) f.b[nt] = 0.0;
+    }
+  };
+  Frag cur, nxt;
+  mbar_wait(&full[0], 0);
+  load(cur, 0, 0);
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % DG_STAGES;
-    mbar_wait(&full[s], (kt / DG_STAGES) & 1);
-    const uint8_t* sa = smem + s * DG_STAGE_BYTES;
-    const uint8_t* sx = sa + DG_A_BYTES;
-    const bool tail = (kt == KT - 1) && (g.K - kt * DG_BK < DG_BK);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int k = dg_kperm(tq, h);
-      double a[2][2], b[8];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int m = wm * 32 + mt * 16 + r * 8 + gq;
-          const int off = TRANS ? m * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3))
-                                : (m >> 4) * 2048 + k * 128 +
-                                      (((((m & 15) >> 1) ^ (k & 7)) << 4) | ((m & 1) << 3));
-          a[mt][r] = *reinterpret_cast<const double*>(sa + off);
+    for (int sub = 0; sub < SUBS; ++sub) {
+      if (sub + 1 < SUBS) {
+        load(nxt, kt, sub + 1);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (kt + 1 < KT) {
+          mbar_wait(&full[(kt + 1) % DG_STAGES], ((kt + 1) / DG_STAGES) & 1);
+          load(nxt, kt + 1, 0);
         }
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-        const int n = wn * 64 + nt * 8 + gq;
-        b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
-      }
-      if (tail && kt * DG_BK + k >= g.K) {
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) a[mt][0] = a[mt][1] = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) b[nt] = 0.0;
       }
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+        for (int nt = 0; nt < DG_NT; ++nt) dmma_16x8x4(acc[mt][nt], cur.a[mt][0], cur.a[mt][1], cur.b[nt]);
+      cur = nxt;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
     // refill the stage released one iteration ago (most likely already drained by all warps)
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + DG_STAGES < KT) {
       const int sp = (kt - 1) % DG_STAGES;
@@ -162,13 +189,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   }
 
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < DG_NT; ++nt)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = n0 + wn * 64 + nt * 8 + 2 * tq + (r & 1);
+        const int row = m0 + wm * DG_WM + mt * 16 + gq + ((r & 2) ? 8 : 0);
+        const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
         if (row < g.M && col < g.N) {
           double v = acc[mt][nt][r];
           if (row >= g.band_lo && row < g.band_hi)

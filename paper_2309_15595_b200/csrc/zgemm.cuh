@@ -63,8 +63,9 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     zgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const ZGemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment for the 128B swizzle, derived from the __shared__ array so every
+  // fragment load stays an LDS (a pointer rebuilt from an integer becomes a generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
   uint64_t* empty = full + ZG_STAGES;
 
@@ -132,60 +133,80 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
 
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % ZG_STAGES;
-    mbar_wait(&full[s], (kt / ZG_STAGES) & 1);
-    const uint8_t* sa = smem + s * ZG_STAGE_BYTES;
-    const uint8_t* sx = sa + ZG_A_BYTES;
-    const bool tail = (kt == KT - 1) && (g.K - kt * ZG_BK < ZG_BK);
+  // Fragments are double-buffered in registers: the loads of sub-step t+1 (including the first
+  // sub-step of the next k-tile, after its full barrier) are issued before the DMMAs of t.
+  constexpr int SUBS = 2 * ZG_KS;                      // m16n8k4 sub-steps per k-tile
+  struct Frag {
+    double2 a[2][2], b[4];
+  };
+  auto load = [&](Frag& f, int kt, int sub) {
+    const int u = sub >> 1, h = sub & 1;
+    const int k = 2 * tq + h;                          // k inside the 8-wide slab u
+    const uint8_t* sa = smem + (kt % ZG_STAGES) * ZG_STAGE_BYTES + u * ZG_A_SLAB;
+    const uint8_t* sx = smem + (kt % ZG_STAGES) * ZG_STAGE_BYTES + ZG_A_BYTES + u * ZG_X_SLAB;
 #pragma unroll
-    for (int hh = 0; hh < 2 * ZG_KS; ++hh) {
-      const int u = hh >> 1, h = hh & 1;
-      const int k = 2 * tq + h;                        // k inside the 8-wide slab u
-      const uint8_t* sau = sa + u * ZG_A_SLAB;
-      const uint8_t* sxu = sx + u * ZG_X_SLAB;
-      double2 a[2][2], b[4];
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int r = 0; r < 2; ++r) {
+        const int m = wm * 32 + mt * 16 + r * 8 + gq;  // m & 7 == gq
+        const int off = CONJ ? m * 128 + ((k ^ gq) << 4)
+                             : (m >> 3) * 1024 + k * 128 + ((gq ^ k) << 4);
+        f.a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
+      }
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int m = wm * 32 + mt * 16 + r * 8 + gq;  // m & 7 == gq
-          const int off = CONJ ? m * 128 + ((k ^ gq) << 4)
-                               : (m >> 3) * 1024 + k * 128 + ((gq ^ k) << 4);
-          a[mt][r] = *reinterpret_cast<const double2*>(sau + off);
-        }
+    for (int nt = 0; nt < 4; ++nt) {
+      const int n = wn * 32 + nt * 8 + gq;
+      f.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
+    }
+    if (kt * ZG_BK + 8 * u + k >= g.K) {               // K tail (the TMA box may hold stale data)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) f.a[mt][0] = f.a[mt][1] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) f.b[nt] = make_double2(0.0, 0.0);
+    }
+  };
+  auto mma = [&](const Frag& f) {
+    // real parts of opA times X
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        const int n = wn * 32 + nt * 8 + gq;
-        b[nt] = *reinterpret_cast<const double2*>(sxu + n * 128 + ((k ^ gq) << 4));
+        dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].x);
+        dmma_16x8x4(acc_im[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].y);
       }
-      if (tail && kt * ZG_BK + 8 * u + k >= g.K) {
+    // imaginary parts: A: re -= Ai*Bi, im += Ai*Br;  A^H: re += Ai*Bi, im -= Ai*Br
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) a[mt][0] = a[mt][1] = make_double2(0.0, 0.0);
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) b[nt] = make_double2(0.0, 0.0);
+      for (int nt = 0; nt < 4; ++nt) {
+        const double bre = CONJ ? f.b[nt].y : -f.b[nt].y;
+        const double bim = CONJ ? -f.b[nt].x : f.b[nt].x;
+        dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].y, f.a[mt][1].y, bre);
+        dmma_16x8x4(acc_im[mt][nt], f.a[mt][0].y, f.a[mt][1].y, bim);
       }
-      // real parts of opA times X
+  };
+
+  Frag cur, nxt;
+  mbar_wait(&full[0], 0);
+  load(cur, 0, 0);
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % ZG_STAGES;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          dmma_16x8x4(acc_re[mt][nt], a[mt][0].x, a[mt][1].x, b[nt].x);
-          dmma_16x8x4(acc_im[mt][nt], a[mt][0].x, a[mt][1].x, b[nt].y);
+    for (int sub = 0; sub < SUBS; ++sub) {
+      if (sub + 1 < SUBS) {
+        load(nxt, kt, sub + 1);
+      } else {
+        // every fragment of stage s is in registers: release it, then prefetch the next tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (kt + 1 < KT) {
+          mbar_wait(&full[(kt + 1) % ZG_STAGES], ((kt + 1) / ZG_STAGES) & 1);
+          load(nxt, kt + 1, 0);
         }
-      // imaginary parts: A: re -= Ai*Bi, im += Ai*Br;  A^H: re += Ai*Bi, im -= Ai*Br
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const double bre = CONJ ? b[nt].y : -b[nt].y;
-          const double bim = CONJ ? -b[nt].x : b[nt].x;
-          dmma_16x8x4(acc_re[mt][nt], a[mt][0].y, a[mt][1].y, bre);
-          dmma_16x8x4(acc_im[mt][nt], a[mt][0].y, a[mt][1].y, bim);
-        }
+      }
+      mma(cur);
+      cur = nxt;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
     // refill the stage released one iteration ago (most likely already drained by all warps)
     if (threadIdx.x == 0 && kt >= 1 && kt - 1 + ZG_STAGES < KT) {
       const int sp = (kt - 1) % ZG_STAGES;
