@@ -194,6 +194,22 @@ chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int myc
 chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols, double cond_est,
                             chase_stats_t* stats, int32_t* info);
 
+/* ---------------------------------------------------------------------------------------
+ * Residuals -- Alg.2 l.23-28: resid[j] = ||H v_j - ritz[j] v_j||_2
+ * for the ncols columns of V (Ritz vectors, C-layout):
+ *   B2 <- Bcast(C, ccomm) (rows [c0, c0+n_c) of V, from the owning rank(s) of the column
+ *   communicator), B <- H C with "B - ritzv B2" fused into the HEMM epilogue of the first rank of
+ *   the column communicator, AllReduce(SUM, ccomm), squared column norms of the local rows,
+ *   AllReduce(SUM, rcomm), sqrt.
+ *  A_local, lda  as for chase_filter (read only).
+ *  V, ldv        device, read only: C-layout block, ncols columns (1..n_max).
+ *  ritz          host, ncols Ritz values (finite).
+ *  resid         host out, ncols residual norms (identical on every rank).
+ * Uses the B-layout workspace (its content is overwritten).  Synchronises the stream once.
+ * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL. */
+chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t lda, const void* V,
+                               int64_t ldv, int64_t ncols, const double* ritz, double* resid);
+
 /* Alg.5, host, pure: t' = (ritz[0]-c)/e, t = (ritz[locked]-c)/e,
  * |rho| = max(|t - sqrt(t^2-1)|, |t + sqrt(t^2-1)|) (complex sqrt: 1 when |t| <= 1),
  * d = degrees[locked], d_M = max(degrees[locked..n-1]); returns |rho|^d |rho'|^(d_M - d).

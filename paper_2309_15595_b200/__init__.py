@@ -33,7 +33,7 @@ EXPORTED = (
     "chase_block_dims", "chase_workspace_size", "chase_set_workspace", "chase_filter",
     "chase_filter_record", "chase_filter_schedule", "chase_cholqr", "chase_cond_est",
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
-    "chase_status_string",
+    "chase_status_string", "chase_residuals",
 )
 
 
@@ -87,6 +87,7 @@ def load() -> ctypes.CDLL:
                                         ctypes.POINTER(chase_step_record_t), ctypes.POINTER(I32), c_i64p]),
         "chase_cholqr": (I32, [V, V, I64, I64, D, ctypes.POINTER(chase_stats_t), ctypes.POINTER(I32)]),
         "chase_cond_est": (D, [ctypes.POINTER(D), I64, D, D, ctypes.POINTER(I32), I64]),
+        "chase_residuals": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "chase_shift_value": (D, [I64, I64, D]),
         "chase_profile_enable": (I32, [V, I32]),
         "chase_profile_read": (I32, [V, ctypes.POINTER(D), c_i64p]),
@@ -233,6 +234,19 @@ def chase_cholqr(h, V, cond_est: float, ncols: int | None = None, raise_on_error
     return {"status": s, "variant": st.qr_variant, "passes": st.qr_passes, "info": info.value}
 
 
+def chase_residuals(h, A_local, V, ritz, ncols: int | None = None):
+    """Residual norms ||A v_j - ritz_j v_j|| (Alg.2 l.23-28) of the columns of V."""
+    a_ptr, lda = _colmajor(A_local, "A_local")
+    v_ptr, ldv = _colmajor(V, "V")
+    ncols = V.shape[1] if ncols is None else ncols
+    r = np.ascontiguousarray(np.asarray(ritz, dtype=np.float64)[:ncols])
+    out = np.empty(ncols, dtype=np.float64)
+    _check(load().chase_residuals(h, a_ptr, lda, v_ptr, ldv, ncols,
+                                  r.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "chase_residuals")
+    return out
+
+
 def chase_cond_est(ritz, c: float, e: float, degrees, locked: int = 0) -> float:
     """Alg.5 over the n = len(degrees) vectors; ritz needs at least n values (ascending)."""
     r = np.ascontiguousarray(np.asarray(ritz, dtype=np.float64))
@@ -293,6 +307,9 @@ class Chase:
 
     def cholqr(self, V, cond_est, ncols=None, raise_on_error=True):
         return chase_cholqr(self.h, V, cond_est, ncols, raise_on_error)
+
+    def residuals(self, A_local, V, ritz, ncols=None):
+        return chase_residuals(self.h, A_local, V, ritz, ncols)
 
     def record(self):
         return chase_filter_record(self.h)

@@ -109,6 +109,9 @@ struct chase_handle_s {
   void* Gws = nullptr;      // n_max x n_max (Gram / R)
   void* Wws = nullptr;      // n_r x n_max (TRSM output)
   void* Rinv = nullptr;     // 64 x n_max (inverted diagonal blocks of R)
+  void* B2ws = nullptr;     // n_c x n_max (C redistributed into B-layout, Alg.2 l.23)
+  double* d_ritz = nullptr;
+  double* d_nrm = nullptr;
   int* d_info = nullptr;
   double* d_shift = nullptr;
   int* h_info = nullptr;    // pinned
@@ -165,7 +168,7 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 struct WsLayout {
-  size_t b, g, w, rinv, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, info, s, total;
 };
 // B-layout block (n_c x n_max) | Gram/R (n_max x n_max) | TRSM output W (n_r x n_max)
 // | inverted diagonal blocks of R (64 x n_max) | info | shift
@@ -177,10 +180,16 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)pad_ld(h->n_c) * h->n_max * es);
   L.g = off;
   off += align256((size_t)pad_ld(h->n_max) * h->n_max * es);
-  L.w = off;
-  off += align256((size_t)pad_ld(h->n_r) * h->n_max * es);
+  L.w = off;                                            // also the residual Bcast staging area
+  off += align256((size_t)(std::max(h->n_r, h->n_c) + 2) * h->n_max * es);
   L.rinv = off;
   off += align256((size_t)TRTRI_NB * (h->n_max + TRTRI_NB) * es);
+  L.b2 = off;                                           // residual: C redistributed to B-layout
+  off += align256((size_t)pad_ld(h->n_c) * h->n_max * es);
+  L.ritz = off;
+  off += align256((size_t)h->n_max * sizeof(double));
+  L.nrm = off;
+  off += align256((size_t)h->n_max * sizeof(double));
   L.info = off;
   off += 256;
   L.s = off;
@@ -255,6 +264,9 @@ struct GemmReq {
   int use_beta, band_lo, band_hi, band_shift, upper_only;
   const int* abort_flag;
   int a3d;                   // NoTrans: tA is the 3D single-box view (a_d0 multiple of a piece)
+  const double* col_shift;   // residual epilogue (Alg.2 l.25): out -= col_shift[n] y2(m, n)
+  const void* y2;
+  int64_t ldy2;
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
@@ -268,6 +280,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
     a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
     a.a3d = r.a3d;
+    a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
   }
   DGemmArgs a;
@@ -279,6 +292,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
   a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
   a.a3d = r.a3d;
+  a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
 }
 
@@ -505,6 +519,9 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->Gws = base + L.g;
   h->Wws = base + L.w;
   h->Rinv = base + L.rinv;
+  h->B2ws = base + L.b2;
+  h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
+  h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
   h->d_info = reinterpret_cast<int*>(base + L.info);
   h->d_shift = reinterpret_cast<double*>(base + L.s);
   return CHASE_OK;
@@ -591,7 +608,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
 
   for (int s = 1; s <= D; ++s) {
     const chase_step_record_t& r = rec[s - 1];
-    GemmReq g;
+    GemmReq g{};
     g.alpha = alpha[s - 1];
     g.beta = beta[s - 1];
     g.c = c;
@@ -858,6 +875,89 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   }
   if (info_out) *info_out = info;
   return st;
+}
+
+// Alg.2 l.23-28: residual norms ||H v_j - lambda_j v_j|| of Ritz pairs.
+chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t lda, const void* V,
+                               int64_t ldv, int64_t ncols, const double* ritz, double* resid) {
+  if (!h || !A_local || !V || !ritz || !resid) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
+  for (int64_t j = 0; j < ncols; ++j)
+    if (!std::isfinite(ritz[j])) return CHASE_EINVAL;
+  if (!h->ws) return CHASE_ESTATE;
+  const size_t es = esize_of(h->dt), per = es / 8;
+  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
+    return CHASE_EINVAL;
+  if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;
+  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
+  const int n = (int)ncols;
+  CUDA_TRY(cudaMemcpyAsync(h->d_ritz, ritz, ncols * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+
+  // l.23 B2 <- Bcast(C2, ccomm): rows [c0, c0+n_c) of V, from the rank(s) of this column
+  // communicator that own them (one Bcast per owning block; a square grid needs one)
+  const char* Vc = static_cast<const char*>(V);
+  char* B2 = static_cast<char*>(h->B2ws);
+  const void* y2 = B2;
+  int64_t ldy2 = ldb;
+  if (h->p == 1 && h->q == 1) {
+    y2 = V;                                           // C- and B-layout coincide on a 1x1 grid
+    ldy2 = ldv;
+  } else {
+    ProfScope ps(h, CAT_ALLREDUCE, 0);
+    char* stage = static_cast<char*>(h->Wws);
+    for (int i2 = 0; i2 < h->p; ++i2) {
+      int64_t nr2, r02;
+      block_part(h->N, h->p, i2, &nr2, &r02);
+      const int64_t lo = std::max(h->c0, r02), hi = std::min(h->c0 + n_c, r02 + nr2);
+      if (lo >= hi) continue;
+      const int64_t rows = hi - lo;
+      if (h->myrow == i2)
+        CUDA_TRY(cudaMemcpy2DAsync(stage, rows * es, Vc + (size_t)(lo - h->r0) * es, ldv * es,
+                                   rows * es, n, cudaMemcpyDeviceToDevice, h->stream));
+      if (h->p > 1)
+        NCCL_TRY(ncclBroadcast(stage, stage, (size_t)rows * n * per, ncclDouble, i2, h->ccomm,
+                               h->stream));
+      CUDA_TRY(cudaMemcpy2DAsync(B2 + (size_t)(lo - h->c0) * es, ldb * es, stage, rows * es,
+                                 rows * es, n, cudaMemcpyDeviceToDevice, h->stream));
+    }
+  }
+  // l.24-25 B <- H C - ritzv B2: the odd-step HEMM with the shift term fused in the epilogue of
+  // the first rank of the column communicator (linear, so it commutes with the AllReduce)
+  CUtensorMap tA_t, tC;
+  STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &tC, V, n_r, n, ldv, ROLE_X));
+  char* Bc = static_cast<char*>(h->Bws);
+  {
+    GemmReq g{};
+    g.conj = true; g.tA = &tA_t; g.tX = &tC;
+    g.M = (int)n_c; g.N = n; g.K = (int)n_r;
+    g.out = Bc; g.ldo = ldb;
+    g.alpha = 1.0; g.beta = 0.0; g.c = 0.0; g.use_beta = 0;
+    g.band_lo = g.band_hi = 0;
+    g.col_shift = h->myrow == 0 ? h->d_ritz : nullptr;
+    g.y2 = y2; g.ldy2 = ldy2;
+    ProfScope ps(h, CAT_HEMM_ODD, 1);
+    STATUS_TRY(run_gemm(h, g));
+  }
+  if (h->p > 1) STATUS_TRY(allreduce(h, Bc, (size_t)ldb * n, h->ccomm));
+  // l.26 squared column norms of the local rows, l.27 AllReduce over rcomm, l.28 sqrt
+  {
+    ProfScope ps(h, CAT_OTHER, 2);
+    if (h->dt == CHASE_C128)
+      colnorm2_kernel<double2><<<n, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(Bc), ldb, (int)n_c, h->d_nrm);
+    else
+      colnorm2_kernel<double><<<n, 256, 0, h->stream>>>(reinterpret_cast<const double*>(Bc), ldb, (int)n_c, h->d_nrm);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (h->q > 1) {
+    ProfScope ps(h, CAT_ALLREDUCE, 0);
+    NCCL_TRY(ncclAllReduce(h->d_nrm, h->d_nrm, n, ncclDouble, ncclSum, h->rcomm, h->stream));
+  }
+  sqrt_kernel<<<(n + 255) / 256, 256, 0, h->stream>>>(h->d_nrm, n);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(resid, h->d_nrm, ncols * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CHASE_OK;
 }
 
 double chase_shift_value(int64_t m, int64_t n, double norm) {

@@ -52,6 +52,9 @@ struct DGemmArgs {
   int upper_only;
   const int* abort_flag;
   int a3d;                 // NoTrans only: tmA is the 3D view {16 doubles, k, m/16} -> 1 TMA/stage
+  const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (Alg.2 l.25)
+  const double* y2;
+  long long ldy2;
 };
 
 __device__ __forceinline__ int dg_kperm(int t, int h) {
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
           double v = acc[mt][nt][r];
           if (row >= g.band_lo && row < g.band_hi)
             v -= g.c * g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+          if (g.col_shift != nullptr) v -= g.col_shift[col] * g.y2[(long long)row + (long long)col * g.ldy2];
           v *= g.alpha;
           double* o = g.out + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) v += g.beta * *o;

@@ -36,6 +36,8 @@ template <typename T> __device__ __forceinline__ T s_real(double r);
 template <> __device__ __forceinline__ double2 s_real<double2>(double r) { return make_double2(r, 0.0); }
 template <> __device__ __forceinline__ double s_real<double>(double r) { return r; }
 __device__ __forceinline__ void s_add_re(double2& a, double v) { a.x += v; }
+__device__ __forceinline__ double s_abs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double s_abs2(double a) { return a * a; }
 __device__ __forceinline__ void s_add_re(double& a, double v) { a += v; }
 
 // One CTA.  G column-major (ld), block rows/cols [kb, kb+nb).  On exit the upper triangle of
@@ -140,6 +142,33 @@ __global__ void __launch_bounds__(TRTRI_NB)
     }
   }
   for (int i = 0; i < TRTRI_NB; ++i) Rinv[(long long)i + (long long)(kb + j) * TRTRI_NB] = X[i][j];
+}
+
+// Residual norms, Alg.2 l.26 "nrm <- SquaredNorm(B)": nrm[c] = sum_r |B[r, c]|^2 over the local
+// rows of the B-layout block.  One CTA per column, fixed-order tree reduction (deterministic).
+template <typename T>
+__global__ void colnorm2_kernel(const T* B, long long ld, int rows, double* nrm) {
+  __shared__ double part[256];
+  const int tid = threadIdx.x;
+  const long long col = blockIdx.x;
+  double acc = 0.0;
+  for (int r = tid; r < rows; r += 256) {
+    const T v = B[(long long)r + col * ld];
+    acc += s_abs2(v);
+  }
+  part[tid] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (tid < w) part[tid] += part[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) nrm[col] = part[0];
+}
+
+// Alg.2 l.28 "resd <- sqrt(nrm)" on the reduced squared norms.
+__global__ void sqrt_kernel(double* v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = sqrt(v[i]);
 }
 
 // Alg.4 l.5-7 on the reduced Gram matrix: norm = sum_j Re G[j][j]; s = 11 (m n + n (n+1)) u norm;

@@ -56,6 +56,9 @@ struct ZGemmArgs {
   int upper_only;          // skip CTAs whose tile lies strictly below the diagonal (m > n)
   const int* abort_flag;   // non-null: skip the whole GEMM when *abort_flag != 0 (POTRF info)
   int a3d;                 // NoTrans only: tmA is the 3D view {8 complex, k, m/8} -> 1 TMA/stage
+  const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (residual,
+  const double2* y2;       //   Alg.2 l.25 "B <- B - ritzv B2" fused into the HEMM epilogue)
+  long long ldy2;
 };
 
 template <bool CONJ>
@@ -230,6 +233,12 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
             const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
             vr -= g.c * x.x;
             vi -= g.c * x.y;
+          }
+          if (g.col_shift != nullptr) {
+            const double2 y = g.y2[(long long)row + (long long)col * g.ldy2];
+            const double lam = g.col_shift[col];
+            vr -= lam * y.x;
+            vi -= lam * y.y;
           }
           vr *= g.alpha;
           vi *= g.alpha;

@@ -51,23 +51,35 @@ def main():
     qr = h.cholqr(Vd, est, raise_on_error=False)
     torch.cuda.synchronize()
     Q = Vd.T.cpu().numpy().T.copy()
+    # residuals (Alg.2 l.23-28) of the orthonormal columns with Rayleigh-quotient values
+    qs = [None] * world
+    dist.all_gather_object(qs, (mycol, r0, n_r, Q))
+    Qg = np.zeros((N, n), dtype=dt)
+    for (j_, rr0, nr_, qq) in qs:
+        if j_ == 0:
+            Qg[rr0:rr0 + nr_] = qq
+    obj = [np.real(np.einsum("ij,ij->j", Qg.conj(), A @ Qg)) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ritz = obj[0]
+    resid = h.residuals(Ad, Vd, ritz)
     g = [None] * world
-    dist.all_gather_object(g, (rank, myrow, mycol, r0, n_r, Vf, Q, rec, mv, qr))
+    dist.all_gather_object(g, (rank, myrow, mycol, r0, n_r, Vf, Q, rec, mv, qr, resid, ritz))
     if rank == 0:
         Vfull = np.zeros((N, n), dtype=dt)
         Qfull = np.zeros((N, n), dtype=dt)
         replica = 0.0
-        for (rk, i, j, rr0, nr, vf, qq, rc, m, qi) in g:
+        for (rk, i, j, rr0, nr, vf, qq, rc, m, qi, rs, rz) in g:
             if j == 0:
                 Vfull[rr0:rr0 + nr] = vf
                 Qfull[rr0:rr0 + nr] = qq
-        for (rk, i, j, rr0, nr, vf, qq, rc, m, qi) in g:
+        for (rk, i, j, rr0, nr, vf, qq, rc, m, qi, rs, rz) in g:
             replica = max(replica, float(np.max(np.abs(vf - Vfull[rr0:rr0 + nr]))),
                           float(np.max(np.abs(qq - Qfull[rr0:rr0 + nr]))))
         np.savez(out, V=Vfull, Q=Qfull, replica=replica, est=est,
                  variants=np.array([x[9]["variant"] for x in g]), passes=np.array([x[9]["passes"] for x in g]),
                  status=np.array([x[9]["status"] for x in g]), mv=np.array([x[8] for x in g]),
-                 recs=np.array([str(x[7]) for x in g]), ranks=np.array([[x[1], x[2], x[4]] for x in g]))
+                 recs=np.array([str(x[7]) for x in g]), ranks=np.array([[x[1], x[2], x[4]] for x in g]),
+                 resid=np.array([x[10] for x in g]), ritz=g[0][11])
     h.close()
     dist.destroy_process_group()
 

@@ -112,3 +112,24 @@ def test_repeatable_bitwise():
     o1, _, _ = gpu_filter(A, V0, d, b, True)
     o2, _, _ = gpu_filter(A, V0, d, b, True)
     assert np.array_equal(o1, o2)
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("N,n", [(61, 9), (300, 40), (512, 60)])
+def test_residuals_match_oracle(complex_, N, n):
+    """chase_residuals (Alg.2 l.23-28, fused -ritzv B2 epilogue) vs oracle.residuals on
+    approximate Ritz pairs (exact eigenvectors + noise, Rayleigh-quotient values)."""
+    import torch
+    lam = ci.uniform_spectrum(N, -2.0, 5.0)
+    Q = ci.haar_unitary(N, N, complex_)
+    A = ci.dense_from_spectrum(lam, N, complex_)
+    noise = ci.gaussian_block(N, n, N + 1, complex_)
+    V = Q[:, :n] + 1e-3 * noise
+    V = np.linalg.qr(V)[0]
+    ritz = np.real(np.einsum("ij,ij->j", V.conj(), A @ V))
+    ref = oracle.residuals(A, V, ritz)
+    h = cb.Chase(cb.CHASE_C128 if complex_ else cb.CHASE_R64, N, n)
+    got = h.residuals(dev(A), dev(V), ritz)
+    torch.cuda.synchronize()
+    h.close()
+    assert np.max(np.abs(got - ref) / np.maximum(ref, 1e-300)) <= 1e-10

@@ -79,6 +79,10 @@ def test_grid_matches_oracle(tmp_path, grid, complex_):
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(n)) <= 1e-12
     kappa = np.linalg.cond(ref)
     assert np.linalg.norm(Q - qref["Q"]) / np.sqrt(n) <= 100 * kappa * 2.0 ** -53 + 1e-13
+    # residuals (Alg.2 l.23-28): identical on every rank, equal to the oracle on the gathered Q
+    rres = oracle.residuals(A, Q, res["ritz"])
+    assert np.all(res["resid"] == res["resid"][0])
+    assert np.max(np.abs(res["resid"][0] - rres) / rres) <= 1e-10
 
 
 FULL = [("C3", (2, 1)), ("C3", (2, 2)), ("C3", (2, 4)), ("C4", (2, 2)), ("C4", (2, 4)),
