@@ -317,6 +317,20 @@ def main():
     hemm_achieved = per_gpu_hemm_flops / launches_per_filter / (hemm_avg_ms / 1e3) / 1e12
     gpu_launches = int(sum(prof_n[k] for k in ("hemm", "gram", "potrf", "trsm", "other")))
 
+    # ---- NEXT-1: residual norms (Alg.2 l.23-28) of the step's output, timed separately
+    ritz = np.sort(lam)[:n]
+    h.residuals(A_local, V, ritz)                     # warm-up
+    barrier()
+    e0.record(stream)
+    resid = h.residuals(A_local, V, ritz)
+    e1.record(stream)
+    barrier()
+    res_ms = allmax(e0.elapsed_time(e1))
+    residual_info = {"ms": res_ms, "unit": "TFLOP/s",
+                     "tflops": (8.0 if w["complex_"] else 2.0) * float(N) ** 2 * n / (res_ms / 1e3) / 1e12,
+                     "max_resid": float(np.max(resid)),
+                     "note": "chase_residuals on the step output (NEXT-1, Alg.2 l.23-28), not part of the step"}
+
     # ---- end-to-end through the public API with host buffers (V in from pinned host, V out)
     e2e = None
     if not args.no_e2e:
@@ -384,6 +398,7 @@ def main():
                          "avg_launch_ms": hemm_avg_ms},
             "profile_ms_per_step": {k: v / args.steps for k, v in prof_ms.items() if k != "reserved"},
             "gpu_launches": gpu_launches,
+            "residuals": residual_info,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -680,7 +680,7 @@ namespace {
 
 template <typename T>
 void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n, int rest) {
-  potrf_diag_kernel<T><<<1, 256, 0, h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info);
+  potrf_diag_kernel<T><<<1, 256, diag_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info);
   h->launches[CAT_POTRF]++;
   if (rest > 0) {
     potrf_panel_kernel<T><<<(rest + PANEL_THREADS - 1) / PANEL_THREADS, PANEL_THREADS,
@@ -772,7 +772,10 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
     h->launches[CAT_TRSM]++;
     // two-level blocking: 64-column diagonal solves inside 256-column panels, so the trailing
     // update of the rest of V runs with K = 256 (4x fewer read-modify-write passes over V)
-    constexpr int OUTER = 256;
+#ifndef CHASE_TRSM_OUTER
+#define CHASE_TRSM_OUTER 512
+#endif
+    constexpr int OUTER = CHASE_TRSM_OUTER;
     auto update = [&](int k0, int kn, int c0, int cn) -> chase_status_t {
       // V[:, c0:c0+cn] -= W[:, k0:k0+kn] R[k0:k0+kn, c0:c0+cn]
       GemmReq g{};
@@ -829,6 +832,8 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   if (!g_qr_attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double2>()));
     CUDA_TRY(cudaFuncSetAttribute(trtri_diag_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trtri_smem<double2>()));
+    CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<double2>()));
+    CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<double>()));
     CUDA_TRY(cudaFuncSetAttribute(trtri_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, trtri_smem<double>()));
     CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double>()));
     g_qr_attr_done = true;

@@ -15,7 +15,7 @@
 
 namespace chase {
 
-constexpr int QR_NB = 32;   // diagonal block size of the blocked POTRF / TRSM
+constexpr int QR_NB = 64;   // diagonal block size of the blocked POTRF
 
 // scalar ops for T = double (real symmetric) or double2 (complex Hermitian)
 __device__ __forceinline__ double2 s_mul(double2 a, double2 b) {
@@ -43,8 +43,11 @@ __device__ __forceinline__ void s_add_re(double& a, double v) { a += v; }
 // One CTA.  G column-major (ld), block rows/cols [kb, kb+nb).  On exit the upper triangle of
 // the block holds R_kk (real positive diagonal).  Unblocked right-looking Cholesky in smem.
 template <typename T>
+constexpr int diag_smem() { return QR_NB * (QR_NB + 1) * (int)sizeof(T); }
+template <typename T>
 __global__ void potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info) {
-  __shared__ T S[QR_NB][QR_NB + 1];   // S[a][b] = G[kb+a, kb+b]
+  extern __shared__ __align__(16) unsigned char qr_dyn[];
+  T (*S)[QR_NB + 1] = reinterpret_cast<T (*)[QR_NB + 1]>(qr_dyn);   // S[a][b] = G[kb+a, kb+b]
   if (*info != 0) return;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int idx = tid; idx < nb * nb; idx += nt) {

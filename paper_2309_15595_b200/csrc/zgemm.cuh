@@ -31,7 +31,13 @@ constexpr int ZG_KS = ZG_KSUB;
 constexpr int ZG_BK = 8 * ZG_KS;  // complex k per stage
 constexpr int ZG_STAGES = 8 / ZG_KS;
 constexpr int ZG_GROUP_M = 8;      // m-tiles per raster group
-constexpr int ZG_CONSUMERS = 8;   // consumer warps (4 along M x 2 along N)
+#ifndef ZG_WARPS_N
+#define ZG_WARPS_N 2              // warps along N (4 along M)
+#endif
+constexpr int ZG_WNW = ZG_WARPS_N;
+constexpr int ZG_CONSUMERS = 4 * ZG_WNW;          // consumer warps
+constexpr int ZG_WN = ZG_BN / ZG_WNW;             // warp tile columns
+constexpr int ZG_NT = ZG_WN / 8;                  // n8 tiles per warp
 constexpr int ZG_THREADS = ZG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
 constexpr int ZG_A_SLAB = ZG_BM * 8 * 16;       // 16 KB per 8-wide k slab
 constexpr int ZG_X_SLAB = ZG_BN * 8 * 16;       // 8 KB per 8-wide k slab
@@ -128,11 +134,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // -------------------------------------------------------------- consumer warps
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  double acc_re[2][4][4], acc_im[2][4][4];
+  double acc_re[2][ZG_NT][4], acc_im[2][ZG_NT][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < ZG_NT; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
 
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // sub-step of the next k-tile, after its full barrier) are issued before the DMMAs of t.
   constexpr int SUBS = 2 * ZG_KS;                      // m16n8k4 sub-steps per k-tile
   struct Frag {
-    double2 a[2][2], b[4];
+    double2 a[2][2], b[ZG_NT];
   };
   auto load = [&](Frag& f, int kt, int sub) {
     const int u = sub >> 1, h = sub & 1;
@@ -157,15 +163,15 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         f.a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
       }
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int n = wn * 32 + nt * 8 + gq;
+    for (int nt = 0; nt < ZG_NT; ++nt) {
+      const int n = wn * ZG_WN + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
     }
     if (kt * ZG_BK + 8 * u + k >= g.K) {               // K tail (the TMA box may hold stale data)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) f.a[mt][0] = f.a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) f.b[nt] = make_double2(0.0, 0.0);
+      for (int nt = 0; nt < ZG_NT; ++nt) f.b[nt] = make_double2(0.0, 0.0);
     }
   };
   auto mma = [&](const Frag& f) {
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
+      for (int nt = 0; nt < ZG_NT; ++nt) {
         dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].x);
         dmma_16x8x4(acc_im[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].y);
       }
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
+      for (int nt = 0; nt < ZG_NT; ++nt) {
         const double bre = CONJ ? f.b[nt].y : -f.b[nt].y;
         const double bim = CONJ ? -f.b[nt].x : f.b[nt].x;
         dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].y, f.a[mt][1].y, bre);
@@ -222,11 +228,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int nt = 0; nt < ZG_NT; ++nt)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = n0 + wn * 32 + nt * 8 + 2 * tq + (r & 1);
+        const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
         if (row < g.M && col < g.N) {
           double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
           if (row >= g.band_lo && row < g.band_hi) {

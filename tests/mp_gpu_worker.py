@@ -17,6 +17,7 @@ from paper_2309_15595_b200 import dist as cdist
 
 def main():
     p, q, N, complex_, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4] == "c", sys.argv[5]
+    pad = int(sys.argv[6]) if len(sys.argv) > 6 else 0        # extra leading-dimension rows
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     assert world == p * q
     torch.cuda.set_device(local)
@@ -36,7 +37,8 @@ def main():
 
     def dev(a):
         rows, cols = a.shape
-        ld = rows + (rows % 2 if not complex_ else 0)
+        ld = rows + pad
+        ld += (ld % 2 if not complex_ else 0)
         buf = np.zeros((cols, ld), dtype=dt)
         buf[:, :rows] = a.T
         return torch.from_numpy(buf).cuda().T[:rows]

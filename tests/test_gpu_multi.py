@@ -44,16 +44,17 @@ def torchrun(nproc, script_args, timeout):
 GRIDS = [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)]
 
 
-@pytest.mark.parametrize("complex_", [True, False])
-@pytest.mark.parametrize("grid", GRIDS)
-def test_grid_matches_oracle(tmp_path, grid, complex_):
+@pytest.mark.parametrize("complex_,grid,pad", [(c, g, 0) for c in (True, False) for g in GRIDS] +
+                         [(True, (1, 2), 6), (False, (1, 2), 5), (True, (2, 2), 6)])
+def test_grid_matches_oracle(tmp_path, grid, complex_, pad):
+    """pad > 0: leading dimensions larger than the local rows (strided AllReduce path)."""
     p, q = grid
     if ngpus() < p * q:
         pytest.skip(f"needs {p * q} GPUs")
     N = 301
     out = str(tmp_path / "res.npz")
     r = torchrun(p * q, [os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N),
-                         "c" if complex_ else "r", out], 600)
+                         "c" if complex_ else "r", out, str(pad)], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = np.load(out)
     degs = sorted([2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20] * 3)
