@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cols", type=int, default=2)
+    ap.add_argument("--comm", default="nccl", choices=["fused", "nccl"],
+                    help="N > 1: filter steps as fused HEMM + NVLink reduction kernels, or HEMM + ncclAllReduce")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -253,6 +255,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
     h = cb.Chase(dtype, N, n, p, q, myrow, mycol, uid, local, stream)
     n_r, n_c, r0, c0 = h.n_r, h.n_c, h.r0, h.c0
+    comm_mode = "none"
+    if world > 1:
+        comm_mode = "nccl"
+        if args.comm == "fused" and w["complex_"]:
+            from paper_2309_15595_b200 import dist as cdist
+            cdist.enable_fused_comm(h)
+            comm_mode = "fused HEMM + NVLink peer-memory reduction"
 
     # ---- inputs, resident in HBM before the timed region
     gen = generator(w, lam)
@@ -382,7 +391,8 @@ def main():
                        "step": "chase_filter + chase_cholqr (Alg.4 variant from Alg.5 estimate)",
                        "l2": "no flush needed: A_local is larger than the 126 MB L2 "
                              f"({16 * n_r * n_c / 1e9:.1f} GB per GPU)",
-                       "parallelism": f"2D block grid {p}x{q}, NCCL allreduce"},
+                       "parallelism": f"2D block grid {p}x{q}",
+                       "filter_comm": comm_mode},
             "pct_of_fp64_peak_per_gpu": 100.0 * value / n_gpus / FP64_PEAK_TFLOPS,
             "filter_only_tflops": F * args.steps / (filt_ms / 1e3) / 1e12,
             "qr": {"variant": qr_info["variant"], "passes": qr_info["passes"],

@@ -132,6 +132,26 @@ chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes);
 chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes);
 
 /* ---------------------------------------------------------------------------------------
+ * Fused compute+collective filter steps (complex double, p*q > 1).  With a symmetric
+ * peer-mapped region set, every filter step whose communicator has more than one member runs as
+ * ONE persistent kernel: the tensor-core HEMM publishes each partial output tile into its own
+ * region, the tile's owner (tile mod m) sums the m partial tiles in fixed member order over
+ * NVLink and stores the result into every member's region (P:149's AllReduce, done tile by tile
+ * inside the GEMM, deterministic and replica-identical).  Without it, steps call ncclAllReduce.
+ *
+ * chase_fused_workspace_size: bytes of the symmetric region (identical on every rank).
+ * chase_set_fused_workspace: local = this rank's region (device, 256-byte aligned, >= size);
+ *   peer_bases[r] = the address at which world rank r's region is mapped in this process
+ *   (peer_bases[my world rank] == local); world = p*q.  Zeroes the region's control words; the
+ *   caller must barrier all ranks after every rank returned and before the next chase_filter.
+ *   local == NULL switches back to NCCL.  Errors: CHASE_EINVAL (real dtype, bad pointers,
+ *   p or q > 8), CHASE_ECUDA.  A peer that never arrives makes chase_filter return CHASE_ECUDA
+ *   after a bounded wait (~10 s) instead of hanging. */
+chase_status_t chase_fused_workspace_size(chase_handle_t h, size_t* bytes);
+chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const uint64_t* peer_bases,
+                                         int world);
+
+/* ---------------------------------------------------------------------------------------
  * Chebyshev filter -- Eq.(1), Alg.1 l.4, Alg.2 l.12, with the
  * damped scalars of S:362 (reading #1):
  *   sigma_1 = e/(mu_1 - c);  V_1 = (sigma_1/e)(A - cI)V_0;

@@ -33,7 +33,8 @@ EXPORTED = (
     "chase_block_dims", "chase_workspace_size", "chase_set_workspace", "chase_filter",
     "chase_filter_record", "chase_filter_schedule", "chase_cholqr", "chase_cond_est",
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
-    "chase_status_string", "chase_residuals",
+    "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
+    "chase_set_fused_workspace",
 )
 
 
@@ -88,6 +89,8 @@ def load() -> ctypes.CDLL:
         "chase_cholqr": (I32, [V, V, I64, I64, D, ctypes.POINTER(chase_stats_t), ctypes.POINTER(I32)]),
         "chase_cond_est": (D, [ctypes.POINTER(D), I64, D, D, ctypes.POINTER(I32), I64]),
         "chase_residuals": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(D)]),
+        "chase_fused_workspace_size": (I32, [V, ctypes.POINTER(ctypes.c_size_t)]),
+        "chase_set_fused_workspace": (I32, [V, V, ctypes.POINTER(ctypes.c_uint64), I32]),
         "chase_shift_value": (D, [I64, I64, D]),
         "chase_profile_enable": (I32, [V, I32]),
         "chase_profile_read": (I32, [V, ctypes.POINTER(D), c_i64p]),
@@ -175,6 +178,22 @@ def chase_set_workspace(h, ws):
     """ws: a CUDA tensor of at least chase_workspace_size(h) bytes (kept alive by the caller)."""
     _check(load().chase_set_workspace(h, ctypes.c_void_p(ws.data_ptr()),
                                       ws.numel() * ws.element_size()), "chase_set_workspace")
+
+
+def chase_fused_workspace_size(h) -> int:
+    b = ctypes.c_size_t()
+    _check(load().chase_fused_workspace_size(h, ctypes.byref(b)), "chase_fused_workspace_size")
+    return b.value
+
+
+def chase_set_fused_workspace(h, local_ptr: int | None, peer_ptrs=None):
+    """peer_ptrs[r] = address of world rank r's symmetric region mapped in this process."""
+    if not local_ptr:
+        _check(load().chase_set_fused_workspace(h, None, None, 0), "chase_set_fused_workspace")
+        return
+    arr = (ctypes.c_uint64 * len(peer_ptrs))(*[int(x) for x in peer_ptrs])
+    _check(load().chase_set_fused_workspace(h, ctypes.c_void_p(local_ptr), arr, len(peer_ptrs)),
+           "chase_set_fused_workspace")
 
 
 def chase_filter(h, A_local, V, degrees, c: float, e: float, bounds, ncols: int | None = None):

@@ -16,6 +16,7 @@
 #include "dgemm.cuh"
 #include "qr_kernels.cuh"
 #include "zgemm.cuh"
+#include "zgemm_fused.cuh"
 
 using namespace chase;
 
@@ -115,6 +116,14 @@ struct chase_handle_s {
   int* d_info = nullptr;
   double* d_shift = nullptr;
   int* h_info = nullptr;    // pinned
+  // fused compute+collective filter (symmetric peer memory); see zgemm_fused.cuh
+  bool fused = false;
+  char* fz_base[FUSED_MAX_MEMBERS * FUSED_MAX_MEMBERS] = {nullptr};   // per world rank
+  int world_size = 1;
+  unsigned fused_ep = 0;
+  unsigned long long fused_delivered = 0;
+  int* d_err = nullptr;
+  int num_sms = 148;
   // bookkeeping of the last filter call
   std::vector<chase_step_record_t> record;
   int64_t last_matvecs = 0;
@@ -201,6 +210,7 @@ static WsLayout ws_layout(const chase_handle_s* h) {
 
 // ==================================================================== GEMM launchers
 static bool g_attr_done[2][2] = {{false, false}, {false, false}};
+static bool g_fused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
@@ -225,6 +235,10 @@ static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorM
   CUDA_TRY(cudaGetLastError());
   return CHASE_OK;
 }
+
+static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
+                                         const CUtensorMap& tX, const struct GemmReq& r,
+                                         const FusedArgs& f, int T);
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a) {
@@ -296,6 +310,36 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
 }
 
+static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
+                                         const CUtensorMap& tX, const GemmReq& r,
+                                         const FusedArgs& f, int T) {
+  if (r.M <= 0 || r.N <= 0) return CHASE_OK;
+  ZGemmArgs a{};
+  a.M = r.M; a.N = r.N; a.K = r.K;
+  a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
+  a.out = static_cast<double2*>(r.out); a.ldo = r.ldo;
+  a.xin = static_cast<const double2*>(r.xin); a.ldx = r.ldx;
+  a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
+  a.use_beta = 0; a.band_lo = r.band_lo; a.band_hi = r.band_hi; a.band_shift = r.band_shift;
+  a.a3d = r.a3d;
+  const int grid = std::min(T, h->num_sms);
+  if (conj) {
+    if (!g_fused_attr[1]) {
+      CUDA_TRY(cudaFuncSetAttribute(zgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
+      g_fused_attr[1] = true;
+    }
+    zgemm_fused_kernel<true><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  } else {
+    if (!g_fused_attr[0]) {
+      CUDA_TRY(cudaFuncSetAttribute(zgemm_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
+      g_fused_attr[0] = true;
+    }
+    zgemm_fused_kernel<false><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CHASE_OK;
+}
+
 // Tensor maps for the three roles a matrix plays in the GEMM (box shapes of zgemm / dgemm).
 enum MapRole { ROLE_A_NOTRANS, ROLE_A_TRANS, ROLE_X };
 // 3D view of a column-major matrix for the NoTrans A tile: dims {one 128-byte row piece,
@@ -359,6 +403,48 @@ static chase_status_t allreduce_cols(chase_handle_s* h, void* buf, int64_t rows,
   }
   NCCL_TRY(ncclGroupEnd());
   return CHASE_OK;
+}
+
+// ==================================================================== fused-comm workspace
+// Symmetric region (identical size and layout on every rank, peer-mapped by the caller):
+//   Cw  C-layout working block  pad(ceil(N/p)) x n_max      (filter even-step outputs)
+//   Bw  B-layout working block  pad(ceil(N/q)) x n_max      (filter odd-step outputs)
+//   P   partial tiles           pad(max rows)  x n_max
+//   flags [tile * m + src] u32  (tiles of the largest step) x max(p, q)
+//   done  u64 delivery counter, err i32
+struct FusedLayout {
+  int64_t ldc, ldb, ldpo, ldpe;
+  size_t cw, bw, po, pe, flags, done, err, total;
+  int64_t tiles_max;
+};
+// Staging areas by step parity (odd steps: p slots of B-layout rows, even: q slots of C-layout
+// rows) so a member pushing step s+1 partials never overwrites slots still being summed for s.
+static FusedLayout fused_layout(const chase_handle_s* h) {
+  FusedLayout L;
+  const int64_t nr_max = (h->N + h->p - 1) / h->p, nc_max = (h->N + h->q - 1) / h->q;
+  const int64_t rows_max = std::max(nr_max, nc_max);
+  L.ldc = pad_ld(nr_max);
+  L.ldb = pad_ld(nc_max);
+  L.ldpo = L.ldb;
+  L.ldpe = L.ldc;
+  L.tiles_max = ((rows_max + ZG_BM - 1) / ZG_BM) * ((h->n_max + ZG_BN - 1) / ZG_BN);
+  size_t off = 0;
+  L.cw = off;
+  off += align256((size_t)L.ldc * h->n_max * 16);
+  L.bw = off;
+  off += align256((size_t)L.ldb * h->n_max * 16);
+  L.po = off;
+  off += align256((size_t)h->p * L.ldpo * h->n_max * 16);
+  L.pe = off;
+  off += align256((size_t)h->q * L.ldpe * h->n_max * 16);
+  L.flags = off;
+  off += align256((size_t)L.tiles_max * std::max(h->p, h->q) * sizeof(unsigned));
+  L.done = off;
+  off += 256;
+  L.err = off;
+  off += 256;
+  L.total = off;
+  return L;
 }
 
 // ==================================================================== schedule (pure)
@@ -527,6 +613,40 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   return CHASE_OK;
 }
 
+chase_status_t chase_fused_workspace_size(chase_handle_t h, size_t* bytes) {
+  if (!h || !bytes) return CHASE_EINVAL;
+  *bytes = fused_layout(h).total;
+  return CHASE_OK;
+}
+
+chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const uint64_t* peer_bases,
+                                         int world) {
+  if (!h) return CHASE_EINVAL;
+  if (!local) {
+    h->fused = false;
+    return CHASE_OK;
+  }
+  if (h->dt != CHASE_C128 || world != h->p * h->q || !peer_bases || world > 64) return CHASE_EINVAL;
+  const int me = h->myrow * h->q + h->mycol;
+  if (peer_bases[me] != reinterpret_cast<uint64_t>(local)) return CHASE_EINVAL;
+  if (h->p > FUSED_MAX_MEMBERS || h->q > FUSED_MAX_MEMBERS) return CHASE_EINVAL;
+  for (int r = 0; r < world; ++r) {
+    if (!peer_bases[r] || (peer_bases[r] & 255)) return CHASE_EINVAL;
+    h->fz_base[r] = reinterpret_cast<char*>(peer_bases[r]);
+  }
+  h->world_size = world;
+  const FusedLayout L = fused_layout(h);
+  // flags, counter and error word start at zero; the caller barriers all ranks before use
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(local) + L.flags, 0, L.total - L.flags, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  CUDA_TRY(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->d_err = reinterpret_cast<int*>(static_cast<char*>(local) + L.err);
+  h->fused_ep = 0;
+  h->fused_delivered = 0;
+  h->fused = true;
+  return CHASE_OK;
+}
+
 chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int mycol, int64_t ncols,
                                      const int32_t* degrees, int32_t max_steps,
                                      chase_step_record_t* rec, int32_t* nsteps,
@@ -596,18 +716,38 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     beta[s - 1] = -sigma_prev * sigma;
   }
 
-  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
+  const int64_t n_r = h->n_r, n_c = h->n_c;
+  // working buffers: NCCL mode filters V in place and uses the B workspace; fused mode runs in
+  // the symmetric region (peers write their reduced tiles straight into it)
+  // CHASE_FUSED_SELF=1: run the fused kernel even for single-member steps (diagnostics: measures
+  // the persistent kernel + epilogue protocol without any peer)
+  static const bool fused_self = getenv("CHASE_FUSED_SELF") != nullptr;
+  const bool fused = h->fused && h->dt == CHASE_C128 && (h->p > 1 || h->q > 1 || fused_self);
+  FusedLayout FL{};
+  char* Cbuf = static_cast<char*>(V);
+  int64_t ldc = ldv;
+  char* Bbuf = static_cast<char*>(h->Bws);
+  int64_t ldb = pad_ld(n_c);
+  const int me_world = h->myrow * h->q + h->mycol;
+  if (fused) {
+    FL = fused_layout(h);
+    Cbuf = h->fz_base[me_world] + FL.cw;
+    ldc = FL.ldc;
+    Bbuf = h->fz_base[me_world] + FL.bw;
+    ldb = FL.ldb;
+    CUDA_TRY(cudaMemcpy2DAsync(Cbuf, ldc * es, V, ldv * es, n_r * es, ncols,
+                               cudaMemcpyDeviceToDevice, h->stream));
+  }
   CUtensorMap tA_nt, tA_t, tC, tB;
   int a3d = 0;
   STATUS_TRY(make_role_map(h, &tA_nt, A_local, n_r, n_c, lda, ROLE_A_NOTRANS, &a3d));
   STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
-  STATUS_TRY(make_role_map(h, &tC, V, n_r, ncols, ldv, ROLE_X));
-  STATUS_TRY(make_role_map(h, &tB, h->Bws, n_c, ncols, ldb, ROLE_X));
-  char* Vc = static_cast<char*>(V);
-  char* Bc = static_cast<char*>(h->Bws);
+  STATUS_TRY(make_role_map(h, &tC, Cbuf, n_r, ncols, ldc, ROLE_X));
+  STATUS_TRY(make_role_map(h, &tB, Bbuf, n_c, ncols, ldb, ROLE_X));
 
   for (int s = 1; s <= D; ++s) {
     const chase_step_record_t& r = rec[s - 1];
+    const bool odd = (s % 2 == 1);
     GemmReq g{};
     g.alpha = alpha[s - 1];
     g.beta = beta[s - 1];
@@ -620,17 +760,17 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     g.a_d0 = 0;
     g.a_d1 = 0;
     g.N = r.k;
-    if (s % 2 == 1) {
+    if (odd) {
       // B_j = alpha (A_ij^H C_i - c band(C_i)) + [i == 0, s > 1] beta B_j
       g.conj = true;
       g.tA = &tA_t;
       g.tX = &tC;
       g.M = (int)n_c;
       g.K = (int)n_r;
-      g.out = Bc + (size_t)r.off * ldb * es;
+      g.out = Bbuf + (size_t)r.off * ldb * es;
       g.ldo = ldb;
-      g.xin = Vc + (size_t)r.off * ldv * es;
-      g.ldx = ldv;
+      g.xin = Cbuf + (size_t)r.off * ldc * es;
+      g.ldx = ldc;
       g.band_lo = r.band_lo;
       g.band_hi = r.band_hi;
       g.band_shift = (int)(h->c0 - h->r0);   // input C row = output B row + c0 - r0
@@ -643,25 +783,79 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.tX = &tB;
       g.M = (int)n_r;
       g.K = (int)n_c;
-      g.out = Vc + (size_t)r.off * ldv * es;
-      g.ldo = ldv;
-      g.xin = Bc + (size_t)r.off * ldb * es;
+      g.out = Cbuf + (size_t)r.off * ldc * es;
+      g.ldo = ldc;
+      g.xin = Bbuf + (size_t)r.off * ldb * es;
       g.ldx = ldb;
       g.band_lo = r.band_lo;
       g.band_hi = r.band_hi;
       g.band_shift = (int)(h->r0 - h->c0);   // input B row = output C row + r0 - c0
       g.use_beta = r.use_beta;
     }
+    const int m = odd ? h->p : h->q;
+    if (fused && (m > 1 || fused_self)) {
+      // one kernel: HEMM + AllReduce over the step's communicator through peer memory
+      FusedArgs f{};
+      f.m = m;
+      f.me = odd ? h->myrow : h->mycol;
+      for (int i = 0; i < m; ++i) {
+        const int w = odd ? i * h->q + h->mycol : h->myrow * h->q + i;
+        char* base = h->fz_base[w];
+        f.P[i] = reinterpret_cast<double2*>(base + (odd ? FL.po : FL.pe));
+        f.out[i] = reinterpret_cast<double2*>(base + (odd ? FL.bw + (size_t)r.off * FL.ldb * es
+                                                          : FL.cw + (size_t)r.off * FL.ldc * es));
+        f.flags[i] = reinterpret_cast<unsigned*>(base + FL.flags);
+        f.done[i] = reinterpret_cast<unsigned long long*>(base + FL.done);
+      }
+      f.ldP = odd ? FL.ldpo : FL.ldpe;
+      f.slot = (long long)f.ldP * h->n_max;
+      f.ep = ++h->fused_ep;
+      f.done_target = h->fused_delivered;
+      f.owner_beta = s > 1 ? 1 : 0;
+      f.err = h->d_err;
+      static const bool plain = getenv("CHASE_FUSED_PLAIN") != nullptr;
+      f.plain = (m == 1 && plain) ? 1 : 0;
+      g.use_beta = 0;                        // the tile owner adds beta * old after the sum
+      const int T = ((g.M + ZG_BM - 1) / ZG_BM) * ((g.N + ZG_BN - 1) / ZG_BN);
+      ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
+      STATUS_TRY(launch_zgemm_fused(h, g.conj, *g.tA, *g.tX, g, f, T));
+      h->fused_delivered += (unsigned long long)T;
+      continue;
+    }
+    if (fused) {
+      // a local step reads what the previous fused step's owners delivered: wait for all of it
+      const FusedLayout& L = FL;
+      fused_wait_kernel<<<1, 1, 0, h->stream>>>(
+          reinterpret_cast<const unsigned long long*>(h->fz_base[me_world] + L.done),
+          h->fused_delivered, h->d_err);
+      CUDA_TRY(cudaGetLastError());
+    }
     {
-      ProfScope ps(h, s % 2 == 1 ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
+      ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
       STATUS_TRY(run_gemm(h, g));
     }
-    if (s % 2 == 1 && h->p > 1) STATUS_TRY(allreduce(h, g.out, (size_t)ldb * r.k, h->ccomm));
-    if (s % 2 == 0 && h->q > 1) {
+    if (fused) continue;                     // single-member communicator: nothing to reduce
+    if (odd && h->p > 1) STATUS_TRY(allreduce(h, g.out, (size_t)ldb * r.k, h->ccomm));
+    if (!odd && h->q > 1) {
       if (ldv == n_r)
         STATUS_TRY(allreduce(h, g.out, (size_t)n_r * r.k, h->rcomm));
       else
         STATUS_TRY(allreduce_cols(h, g.out, n_r, ldv, r.k, h->rcomm));
+    }
+  }
+  if (fused) {
+    // every tile of the last step delivered here, then the result leaves the symmetric buffer
+    char* base = h->fz_base[me_world];
+    fused_wait_kernel<<<1, 1, 0, h->stream>>>(reinterpret_cast<const unsigned long long*>(base + FL.done),
+                                              h->fused_delivered, h->d_err);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy2DAsync(V, ldv * es, Cbuf, ldc * es, n_r * es, ncols,
+                               cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(h->h_info, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (*h->h_info != 0) {
+      fprintf(stderr, "[chase] fused filter: peer wait timed out\n");
+      return CHASE_ECUDA;
     }
   }
   h->record = rec;

@@ -1,0 +1,373 @@
+// zgemm_fused.cuh -- the filter step as ONE kernel: tensor-core HEMM + the AllReduce of its
+// result over the reducing communicator, done tile by tile over NVLink peer memory.
+//
+// A filter step on a p x q grid is "partial_r = alpha (A_r^(H) X - c band) on every member r of
+// the row (even step) / column (odd step) communicator, then AllReduce(SUM)" (Alg.2 l.12).
+// Here every member runs a persistent grid (one CTA per SM, identical tile sequence on all
+// members).  After the K loop of output tile t a CTA
+//   1. pushes its partial tile into its slot of the tile owner's staging area (NVLink stores;
+//      the owner rotates along each CTA's tile sequence so owner work is spread evenly),
+//   2. releases a per-(tile, member) arrival flag in the owner's memory,
+// and, if it is the owner, waits for the m flags of t, sums the m partial tiles from its LOCAL
+// slots in fixed member order (deterministic, identical bits on every member), adds
+// beta * V_{s-2} (replicated, read locally), pushes the result into the output buffer of every
+// member and bumps each member's delivery counter.  The next step's kernel waits
+// until its delivery counter covers the whole previous step.  The reduction traffic of tile t
+// overlaps the math of the tiles that follow it -- no separate collective launch.
+//
+// Deadlock freedom: all CTAs are co-resident (grid <= #SMs, 1 CTA/SM) and every member walks the
+// same tile sequence per CTA; a partial is always published before its producer waits on
+// anything, so the wait at sequence position i only depends on positions <= i of the peers.
+// Every spin is bounded (~10 s at 2 GHz); on timeout the kernel sets *err and gives up so a
+// broken peer can never hang the GPU.
+#pragma once
+#include "zgemm.cuh"
+
+namespace chase {
+
+constexpr int FUSED_MAX_MEMBERS = 8;
+
+struct FusedArgs {
+  int m;                                     // communicator members (2..8)
+  int me;                                    // my index in the communicator
+  double2* P[FUSED_MAX_MEMBERS];             // staging area of each member: m slots of ldP x n
+  long long slot;                            // elements per slot
+  double2* out[FUSED_MAX_MEMBERS];           // output buffer of each member (ld = g.ldo)
+  unsigned* flags[FUSED_MAX_MEMBERS];        // arrival flags of each member: [tile * m + src]
+  unsigned long long* done[FUSED_MAX_MEMBERS];  // delivery counter of each member
+  long long ldP;
+  unsigned ep;                               // epoch (unique per launch) written into flags
+  unsigned long long done_target;            // wait for *done[me] >= done_target first
+  int owner_beta;                            // owner adds beta * out(old) before broadcasting
+  int* err;                                  // set on a spin timeout
+  int plain;                                 // diagnostics: local epilogue, no protocol (m == 1)
+};
+
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr long long FUSED_SPIN_CYCLES = 20000000000LL;   // ~10 s at 2 GHz
+
+template <bool CONJ>
+__global__ void __launch_bounds__(ZG_THREADS, 1)
+    zgemm_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                       const ZGemmArgs g, const FusedArgs f) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
+  uint64_t* empty = full + ZG_STAGES;
+  __shared__ int s_abort;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
+  const int T = n_tiles * m_tiles;
+  const int my_tiles = (T - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int KT = (g.K + ZG_BK - 1) / ZG_BK;
+  const int L = my_tiles * KT;                        // k-tiles this CTA streams
+  auto tile_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
+  auto tile_origin = [&](int t, int& m0, int& n0) {  // grouped rasterisation as in zgemm
+    const int group = t / (ZG_GROUP_M * n_tiles);
+    const int first_m = group * ZG_GROUP_M;
+    const int gm = min(ZG_GROUP_M, m_tiles - first_m);
+    const int within = t - group * ZG_GROUP_M * n_tiles;
+    m0 = (first_m + within % gm) * ZG_BM;
+    n0 = (within / gm) * ZG_BN;
+  };
+
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    // inputs of this step are complete once every owner of the previous step has delivered
+    const long long t0 = clock64();
+    while (ld_acquire_sys_u64(f.done[f.me]) < f.done_target) {
+      __nanosleep(256);
+      if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+        atomicExch(f.err, 1);
+        s_abort = 1;
+        break;
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // peer stores -> TMA reads
+    for (int s = 0; s < ZG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], ZG_CONSUMERS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (s_abort || L == 0) return;
+
+  // k-tile stream: issue() is called by thread 0 for gs = 0, 1, 2, ... in order, so the
+  // (tile, kt, m0, n0) of the next load are advanced incrementally (no per-k-tile division)
+  int is_seq = 0, is_kt = 0, is_m0 = 0, is_n0 = 0;
+  if (threadIdx.x == 0) tile_origin(tile_of(0), is_m0, is_n0);
+  auto issue = [&](int s) {
+    const int kt = is_kt, m0 = is_m0, n0 = is_n0;
+    mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
+    uint8_t* sa = smem + s * ZG_STAGE_BYTES;
+    uint8_t* sx = sa + ZG_A_BYTES;
+#pragma unroll
+    for (int u = 0; u < ZG_KS; ++u) {
+      const int k0 = kt * ZG_BK + 8 * u;
+      uint8_t* sau = sa + u * ZG_A_SLAB;
+      if (CONJ) {
+        tma_load_2d(sau, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
+      } else if (g.a3d) {
+        tma_load_3d(sau, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 8, &full[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < ZG_BM / 8; ++b)
+          tma_load_2d(sau + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+      }
+      tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
+    }
+    if (++is_kt == KT) {
+      is_kt = 0;
+      if (++is_seq < my_tiles) tile_origin(tile_of(is_seq), is_m0, is_n0);
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmX);
+    for (int gs = 0; gs < ZG_STAGES && gs < L; ++gs) issue(gs);
+  }
+
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc_re[2][ZG_NT][4], acc_im[2][ZG_NT][4];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < ZG_NT; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
+  };
+  zero_acc();
+
+  constexpr int SUBS = 2 * ZG_KS;
+  struct Frag {
+    double2 a[2][2], b[ZG_NT];
+  };
+  auto load = [&](Frag& fr, int gs, int kt, int sub) {
+    const int u = sub >> 1, h = sub & 1;
+    const int k = 2 * tq + h;
+    const uint8_t* sa = smem + (gs % ZG_STAGES) * ZG_STAGE_BYTES + u * ZG_A_SLAB;
+    const uint8_t* sx = smem + (gs % ZG_STAGES) * ZG_STAGE_BYTES + ZG_A_BYTES + u * ZG_X_SLAB;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int m = wm * 32 + mt * 16 + r * 8 + gq;
+        const int off = CONJ ? m * 128 + ((k ^ gq) << 4) : (m >> 3) * 1024 + k * 128 + ((gq ^ k) << 4);
+        fr.a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
+      }
+#pragma unroll
+    for (int nt = 0; nt < ZG_NT; ++nt) {
+      const int n = wn * ZG_WN + nt * 8 + gq;
+      fr.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
+    }
+    if (kt * ZG_BK + 8 * u + k >= g.K) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) fr.a[mt][0] = fr.a[mt][1] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nt = 0; nt < ZG_NT; ++nt) fr.b[nt] = make_double2(0.0, 0.0);
+    }
+  };
+  auto mma = [&](const Frag& fr) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < ZG_NT; ++nt) {
+        dmma_16x8x4(acc_re[mt][nt], fr.a[mt][0].x, fr.a[mt][1].x, fr.b[nt].x);
+        dmma_16x8x4(acc_im[mt][nt], fr.a[mt][0].x, fr.a[mt][1].x, fr.b[nt].y);
+      }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < ZG_NT; ++nt) {
+        const double bre = CONJ ? fr.b[nt].y : -fr.b[nt].y;
+        const double bim = CONJ ? -fr.b[nt].x : fr.b[nt].x;
+        dmma_16x8x4(acc_re[mt][nt], fr.a[mt][0].y, fr.a[mt][1].y, bre);
+        dmma_16x8x4(acc_im[mt][nt], fr.a[mt][0].y, fr.a[mt][1].y, bim);
+      }
+  };
+
+  // epilogue of tile t: publish the partial, and reduce + broadcast it if this member owns t
+  auto epilogue = [&](int t) {
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    if (f.plain) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < ZG_NT; ++nt)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
+            const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
+            if (row < g.M && col < g.N) {
+              double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
+              if (row >= g.band_lo && row < g.band_hi) {
+                const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+                vr -= g.c * x.x;
+                vi -= g.c * x.y;
+              }
+              vr *= g.alpha;
+              vi *= g.alpha;
+              double2* o = f.out[f.me] + (long long)row + (long long)col * g.ldo;
+              if (f.owner_beta) {
+                const double2 old = *o;
+                vr += g.beta * old.x;
+                vi += g.beta * old.y;
+              }
+              *o = make_double2(vr, vi);
+            }
+          }
+      if (threadIdx.x == 0) atomicAdd(f.done[f.me], 1ull);
+      return;
+    }
+    // owner rotates along the CTA's tile sequence (t / gridDim) so every CTA owns 1/m of its tiles
+    const int owner = (t / (int)gridDim.x) % f.m;
+    double2* slot = f.P[owner] + (long long)f.me * f.slot;        // my slot at the owner
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < ZG_NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
+          if (row < g.M && col < g.N) {
+            double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
+            if (row >= g.band_lo && row < g.band_hi) {
+              const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+              vr -= g.c * x.x;
+              vi -= g.c * x.y;
+            }
+            slot[(long long)row + (long long)col * f.ldP] = make_double2(vr * g.alpha, vi * g.alpha);
+          }
+        }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
+    if (owner != f.me) return;
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      for (int src = 0; src < f.m && !s_abort; ++src) {
+        while (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) {
+          __nanosleep(64);
+          if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+            atomicExch(f.err, 1);
+            s_abort = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    // coalesced pass over the tile (column-major 128 x 64), partials read from local slots;
+    // 8 elements per thread per batch so the loads of a batch are all in flight together
+    const double2* __restrict__ mine = f.P[f.me];
+    constexpr int PER = ZG_BM * ZG_BN / ZG_THREADS;     // 32 elements per thread
+    constexpr int BATCH = 8;
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER; b0 += BATCH) {
+      double2 sum[BATCH];
+      long long io[BATCH];
+      bool ok[BATCH];
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i) {
+        const int e = threadIdx.x + (b0 + i) * ZG_THREADS;
+        const int row = m0 + (e % ZG_BM), col = n0 + (e / ZG_BM);
+        ok[i] = row < g.M && col < g.N;
+        const long long ip = (long long)row + (long long)col * f.ldP;
+        io[i] = (long long)row + (long long)col * g.ldo;
+        sum[i] = ok[i] ? mine[ip] : make_double2(0.0, 0.0);
+        for (int src = 1; src < f.m; ++src) {
+          const double2 v = ok[i] ? mine[(long long)src * f.slot + ip] : make_double2(0.0, 0.0);
+          sum[i].x += v.x;
+          sum[i].y += v.y;
+        }
+        if (f.owner_beta && ok[i]) {
+          const double2 old = f.out[f.me][io[i]];
+          sum[i].x += g.beta * old.x;
+          sum[i].y += g.beta * old.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i)
+        if (ok[i])
+          for (int dst = 0; dst < f.m; ++dst) f.out[dst][io[i]] = sum[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+  };
+
+  Frag cur, nxt;
+  mbar_wait(&full[0], 0);
+  load(cur, 0, 0, 0);
+  int kt = 0;                                          // k-tile of gs inside its output tile
+  for (int gs = 0; gs < L; ++gs) {
+    const int s = gs % ZG_STAGES;
+#pragma unroll
+    for (int sub = 0; sub < SUBS; ++sub) {
+      if (sub + 1 < SUBS) {
+        load(nxt, gs, kt, sub + 1);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (gs + 1 < L) {
+          mbar_wait(&full[(gs + 1) % ZG_STAGES], ((gs + 1) / ZG_STAGES) & 1);
+          load(nxt, gs + 1, kt + 1 == KT ? 0 : kt + 1, 0);
+        }
+      }
+      mma(cur);
+      cur = nxt;
+    }
+    if (threadIdx.x == 0 && gs >= 1 && gs - 1 + ZG_STAGES < L) {
+      const int sp = (gs - 1) % ZG_STAGES;
+      mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
+      issue(sp);
+    }
+    if (kt == KT - 1) {
+      epilogue(tile_of(gs / KT));
+      kt = -1;
+      zero_acc();
+      if (s_abort) {
+        // drain: the TMA loads already issued must land before the CTA exits
+        for (int r = gs + 1; r < L && r < gs + ZG_STAGES; ++r)
+          mbar_wait(&full[r % ZG_STAGES], (r / ZG_STAGES) & 1);
+        return;
+      }
+    }
+    ++kt;
+  }
+}
+
+// Waits (one thread) until *done >= target: the last step's tiles are all delivered before the
+// result is copied out of the symmetric buffer.
+__global__ void fused_wait_kernel(const unsigned long long* done, unsigned long long target, int* err) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys_u64(done) < target) {
+    __nanosleep(256);
+    if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+      atomicExch(err, 1);
+      return;
+    }
+  }
+}
+
+}  // namespace chase

@@ -28,3 +28,31 @@ def share_unique_id(get_id, group=None) -> bytes:
     obj = [get_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def enable_fused_comm(chase, group=None):
+    """Give a Chase handle a symmetric peer-mapped region (torch symmetric memory over the world
+    group: device memory + IPC mappings only) so its filter steps run as fused HEMM + NVLink
+    reduction kernels (include/chase.h chase_set_fused_workspace).  Collective over the group."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+
+    import paper_2309_15595_b200 as cb
+
+    group = group or dist.group.WORLD
+    nbytes = cb.chase_fused_workspace_size(chase.h)
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=chase.device)
+    hdl = symm.rendezvous(buf, group)
+    ptrs = [int(x) for x in hdl.buffer_ptrs]
+    cb.chase_set_fused_workspace(chase.h, buf.data_ptr(), ptrs)
+    torch.cuda.synchronize(chase.device)
+    dist.barrier(group)
+    chase._fused_keepalive = (buf, hdl)
+    return hdl
+
+
+def disable_fused_comm(chase):
+    import paper_2309_15595_b200 as cb
+
+    cb.chase_set_fused_workspace(chase.h, None)

@@ -44,17 +44,19 @@ def torchrun(nproc, script_args, timeout):
 GRIDS = [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)]
 
 
-@pytest.mark.parametrize("complex_,grid,pad", [(c, g, 0) for c in (True, False) for g in GRIDS] +
-                         [(True, (1, 2), 6), (False, (1, 2), 5), (True, (2, 2), 6)])
-def test_grid_matches_oracle(tmp_path, grid, complex_, pad):
-    """pad > 0: leading dimensions larger than the local rows (strided AllReduce path)."""
+@pytest.mark.parametrize("complex_,grid,pad,mode", [(c, g, 0, "nccl") for c in (True, False) for g in GRIDS] +
+                         [(True, (1, 2), 6, "nccl"), (False, (1, 2), 5, "nccl"), (True, (2, 2), 6, "nccl")] +
+                         [(True, g, 0, "fused") for g in GRIDS] + [(True, (1, 2), 6, "fused")])
+def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode):
+    """pad > 0: leading dimensions larger than the local rows (strided AllReduce path).
+    mode "fused": filter steps as one HEMM + NVLink peer-memory reduction kernel."""
     p, q = grid
     if ngpus() < p * q:
         pytest.skip(f"needs {p * q} GPUs")
     N = 301
     out = str(tmp_path / "res.npz")
     r = torchrun(p * q, [os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N),
-                         "c" if complex_ else "r", out, str(pad)], 600)
+                         "c" if complex_ else "r", out, str(pad), mode], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = np.load(out)
     degs = sorted([2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20] * 3)
@@ -68,6 +70,7 @@ def test_grid_matches_oracle(tmp_path, grid, complex_, pad):
     err = np.max(np.linalg.norm(V - ref, axis=0) / np.linalg.norm(ref, axis=0))
     assert err <= 1e-10
     assert float(res["replica"]) == 0.0                       # identical bits on all replicas
+    assert np.all(res["repeat_equal"])                        # bitwise repeatable
     assert np.all(res["mv"] == sum(degs))
     for (i, j, nr), recs in zip(res["ranks"], res["recs"]):
         n_r, n_c, _, _ = ci.block_dims(N, p, q, int(i), int(j))
