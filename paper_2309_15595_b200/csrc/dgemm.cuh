@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       cur = nxt;
     }
     // refill the stage released one iteration ago (most likely already drained by all warps)
-    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + DG_STAGES < KT) {
+    // the refill duty rotates over the warps so no single warp carries the producer work
+    if (lane == 0 && warp == (kt & (DG_CONSUMERS - 1)) && kt >= 1 && kt - 1 + DG_STAGES < KT) {
       const int sp = (kt - 1) % DG_STAGES;
       mbar_wait(&empty[sp], ((kt - 1) / DG_STAGES) & 1);
       issue(kt - 1 + DG_STAGES, sp);

@@ -38,7 +38,13 @@ constexpr int ZG_WNW = ZG_WARPS_N;
 constexpr int ZG_CONSUMERS = 4 * ZG_WNW;          // consumer warps
 constexpr int ZG_WN = ZG_BN / ZG_WNW;             // warp tile columns
 constexpr int ZG_NT = ZG_WN / 8;                  // n8 tiles per warp
-constexpr int ZG_THREADS = ZG_CONSUMERS * 32;   // no dedicated producer warp: 9 warps would cap registers at 168
+#ifndef ZG_WS
+#define ZG_WS 0                   // 1: producer warpgroup + setmaxnreg (warp specialisation)
+#endif
+// ZG_WS == 0: no dedicated producer warp (9 warps would cap registers at 168); the refill duty
+// rotates over the 8 MMA warps.  ZG_WS == 1: a 4-warp producer group drops to 40 registers with
+// setmaxnreg and the two MMA warpgroups rise to 232.
+constexpr int ZG_THREADS = (ZG_CONSUMERS + (ZG_WS ? 4 : 0)) * 32;
 constexpr int ZG_A_SLAB = ZG_BM * 8 * 16;       // 16 KB per 8-wide k slab
 constexpr int ZG_X_SLAB = ZG_BN * 8 * 16;       // 8 KB per 8-wide k slab
 constexpr int ZG_A_BYTES = ZG_A_SLAB * ZG_KS;
@@ -125,14 +131,33 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
   };
+#if ZG_WS
+  if (warp < 4) {                                  // producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmX);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % ZG_STAGES;
+        if (kt >= ZG_STAGES) mbar_wait(&empty[s], ((kt / ZG_STAGES) & 1) ^ 1);
+        issue(kt, s);
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  const int cwarp = warp - 4;
+#else
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmX);
     for (int kt = 0; kt < ZG_STAGES && kt < KT; ++kt) issue(kt, kt);
   }
+  const int cwarp = warp;
+#endif
 
   // -------------------------------------------------------------- consumer warps
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = cwarp & 3, wn = cwarp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
   double acc_re[2][ZG_NT][4], acc_im[2][ZG_NT][4];
 #pragma unroll
@@ -217,7 +242,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       cur = nxt;
     }
     // refill the stage released one iteration ago (most likely already drained by all warps)
-    if (threadIdx.x == 0 && kt >= 1 && kt - 1 + ZG_STAGES < KT) {
+    // the refill duty rotates over the warps so no single warp carries the producer work
+    if (!ZG_WS && lane == 0 && warp == (kt & (ZG_CONSUMERS - 1)) && kt >= 1 && kt - 1 + ZG_STAGES < KT) {
       const int sp = (kt - 1) % ZG_STAGES;
       mbar_wait(&empty[sp], ((kt - 1) / ZG_STAGES) & 1);
       issue(kt - 1 + ZG_STAGES, sp);
