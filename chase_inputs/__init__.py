@@ -38,7 +38,7 @@ __all__ = [
     "uniform_spectrum", "clement_spectrum", "wilkinson_spectrum", "haar_unitary",
     "dense_from_spectrum", "DftPhase", "dft_phase", "HartleySign", "hartley_sign",
     "gaussian_block", "Bounds", "bounds_from_spectrum", "block_dims", "uniform_degrees",
-    "ramp_degrees", "CONFIGS", "Config", "svd_synthesized",
+    "ramp_degrees", "CONFIGS", "Config", "svd_synthesized", "cyclic_indices",
 ]
 
 
@@ -119,6 +119,10 @@ class DftPhase:
         Returns a tensor T of shape (nc, nr) (row-major storage of the transpose) so that
         T.data_ptr() is the column-major block with leading dimension nr.
         """
+        return self.block_idx(np.arange(r0, r0 + nr), np.arange(c0, c0 + nc), device, chunk_cols)
+
+    def block_idx(self, rows, cols, device="cpu", chunk_cols: int = 2048):
+        """A[rows][:, cols] for arbitrary global index arrays (block-cyclic blocks), same layout."""
         import torch
 
         dev = torch.device(device)
@@ -126,13 +130,16 @@ class DftPhase:
         pi = torch.from_numpy(np.ascontiguousarray(self.phi.imag)).to(dev)
         ar = torch.from_numpy(np.ascontiguousarray(self.a.real)).to(dev)
         ai = torch.from_numpy(np.ascontiguousarray(self.a.imag)).to(dev)
+        rows_t = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dev)
+        cols_t = torch.as_tensor(np.asarray(cols, dtype=np.int64), device=dev)
+        nr, nc = rows_t.numel(), cols_t.numel()
         out = torch.empty((nc, nr), dtype=torch.complex128, device=dev)
         ov = torch.view_as_real(out)
-        r = torch.arange(r0, r0 + nr, device=dev, dtype=torch.int64)
+        r = rows_t
         N = self.N
         for j0 in range(0, nc, chunk_cols):
             j1 = min(nc, j0 + chunk_cols)
-            s = torch.arange(c0 + j0, c0 + j1, device=dev, dtype=torch.int64)
+            s = cols_t[j0:j1]
             R = r[None, :]            # (1, nr)
             S = s[:, None]            # (cols, 1)
             # canonical pair (lo, hi) = (min, max): value = phi_lo conj(phi_hi) a[(lo-hi) mod N],
@@ -190,18 +197,24 @@ class HartleySign:
         = ac[(r-s) mod N] + as_[(r+s) mod N]  (product-to-sum identity).  Symmetric in (r, s)
         by construction because ac is mirrored and (r+s) is symmetric.
         """
+        return self.block_idx(np.arange(r0, r0 + nr), np.arange(c0, c0 + nc), device, chunk_cols)
+
+    def block_idx(self, rows, cols, device="cpu", chunk_cols: int = 4096):
+        """A[rows][:, cols] for arbitrary global index arrays (block-cyclic blocks)."""
         import torch
 
         dev = torch.device(device)
         sg = torch.from_numpy(self.sign).to(dev)
         ac = torch.from_numpy(self.ac).to(dev)
         as_ = torch.from_numpy(self.as_).to(dev)
+        r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dev)
+        cols_t = torch.as_tensor(np.asarray(cols, dtype=np.int64), device=dev)
+        nr, nc = r.numel(), cols_t.numel()
         out = torch.empty((nc, nr), dtype=torch.float64, device=dev)
-        r = torch.arange(r0, r0 + nr, device=dev, dtype=torch.int64)
         N = self.N
         for j0 in range(0, nc, chunk_cols):
             j1 = min(nc, j0 + chunk_cols)
-            s = torch.arange(c0 + j0, c0 + j1, device=dev, dtype=torch.int64)
+            s = cols_t[j0:j1]
             R = r[None, :]
             S = s[:, None]
             val = ac[torch.remainder(R - S, N)] + as_[torch.remainder(R + S, N)]
@@ -281,6 +294,13 @@ def block_dims(N: int, p: int, q: int, i: int, j: int):
     n_r, r0 = part(N, p, i)
     n_c, c0 = part(N, q, j)
     return n_r, n_c, r0, c0
+
+
+def cyclic_indices(N: int, P: int, k: int, nb: int) -> np.ndarray:
+    """Global indices owned by grid row/column k of P under the block-cyclic distribution with
+    block size nb (P:113): g with (g // nb) % P == k, increasing."""
+    g = np.arange(N)
+    return g[(g // nb) % P == k]
 
 
 def uniform_degrees(n: int, d: int) -> np.ndarray:

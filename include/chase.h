@@ -109,10 +109,32 @@ chase_status_t chase_create(chase_handle_t* h, chase_dtype_t dt, int64_t N, int6
                             int q, int myrow, int mycol, const uint8_t id[128], int device,
                             void* cuda_stream);
 
+/* Block-cyclic distribution ("either a block distribution or a block-cyclic
+ * distribution"; C is distributed over each column communicator with the same block
+ * size): grid row k owns the global rows g with (g / nb) mod p == k, in increasing order, and
+ * likewise grid column k the global columns with (g / nb) mod q == k.  A_local holds
+ * A[rows, cols] of those index sets, V the rows of the same row set.  The -cI shift is applied
+ * through per-row maps of the diagonal (the band of chase_step_record_t is reported as
+ * [-1, -1)).  nb == 0 is the block distribution of chase_create.  Errors as chase_create, plus
+ * CHASE_EINVAL when nb < 0 or a grid row/column would own no block (N < nb * max(p, q)). */
+chase_status_t chase_create_cyclic(chase_handle_t* h, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                   int p, int q, int myrow, int mycol, int64_t nb,
+                                   const uint8_t id[128], int device, void* cuda_stream);
+
+/* Global indices of this rank's local rows (n_r entries) and columns (n_c entries), host
+ * arrays; either may be NULL.  For the block distribution these are r0.. and c0.. */
+chase_status_t chase_local_indices(chase_handle_t h, int64_t* rows, int64_t* cols);
+
+/* Pure host function: the global indices grid row/column k of P owns under block-cyclic
+ * distribution with block nb (idx may be NULL to query *count only). */
+chase_status_t chase_cyclic_indices(int64_t N, int P, int k, int64_t nb, int64_t* idx,
+                                    int64_t* count);
+
 /* Change the stream later calls enqueue on. */
 chase_status_t chase_set_stream(chase_handle_t h, void* cuda_stream);
 
-/* Local block geometry of this rank: A_local is n_r x n_c, rows r0.., columns c0.. of A. */
+/* Local block geometry of this rank: A_local is n_r x n_c, rows r0.., columns c0.. of A
+ * (r0 = c0 = -1 under the block-cyclic distribution; see chase_local_indices). */
 chase_status_t chase_local_dims(chase_handle_t h, int64_t* n_r, int64_t* n_c, int64_t* r0,
                                 int64_t* c0);
 

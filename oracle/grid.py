@@ -29,47 +29,61 @@ def _part(N, P, k):
     return b + (1 if k < rem else 0), k * b + min(k, rem)
 
 
-def distributed_filter(A, V0, degrees, c, e, mu_1, p, q):
+def _owned(N, P, k, nb):
+    """Global indices of grid row/column k: block distribution (nb == 0, remainder rule S:102) or
+    block-cyclic with block nb."""
+    if nb == 0:
+        size, start = _part(N, P, k)
+        return np.arange(start, start + size)
+    g = np.arange(N)
+    return g[(g // nb) % P == k]
+
+
+def distributed_filter(A, V0, degrees, c, e, mu_1, p, q, nb=0):
+    """nb > 0: block-cyclic distribution; the diagonal share of rank (i, j) is then the set of
+    global indices owned both as a row (grid row i) and as a column (grid column j)."""
     d = _check_degrees(degrees)
     N, n = V0.shape
     D = max(d)
     alpha, beta, _ = chebyshev_scalars(c, e, mu_1, D)
-    rows = [_part(N, p, i) for i in range(p)]     # (n_r, r0)
-    cols = [_part(N, q, j) for j in range(q)]     # (n_c, c0)
+    R = [_owned(N, p, i, nb) for i in range(p)]
+    Cc = [_owned(N, q, j, nb) for j in range(q)]
     dtype = np.result_type(A.dtype, V0.dtype)
-    C = [np.array(V0[r0:r0 + nr], dtype=dtype) for (nr, r0) in rows]     # C_i (per grid row)
-    B = [np.zeros((nc, n), dtype=dtype) for (nc, c0) in cols]           # B_j (per grid column)
+    C = [np.array(V0[ri], dtype=dtype) for ri in R]                      # C_i (per grid row)
+    B = [np.zeros((len(cj), n), dtype=dtype) for cj in Cc]              # B_j (per grid column)
     for s in range(1, D + 1):
         k = sum(1 for dj in d if dj >= s)
         off = n - k
         if s % 2 == 1:
-            for j, (nc, c0) in enumerate(cols):
+            for j, cj in enumerate(Cc):
                 acc = None
-                for i, (nr, r0) in enumerate(rows):
-                    Aij = A[r0:r0 + nr, c0:c0 + nc]
+                for i, ri in enumerate(R):
+                    Aij = A[np.ix_(ri, cj)]
                     Ci = C[i][:, off:]
                     part = Aij.conj().T @ Ci
-                    lo, hi = max(r0, c0), min(r0 + nr, c0 + nc)
-                    if lo < hi:
-                        part[lo - c0:hi - c0] -= c * Ci[lo - r0:hi - r0]
+                    # diagonal share: B rows (global cj) that are also local C rows (global ri)
+                    _, ob, oc = np.intersect1d(cj, ri, return_indices=True)
+                    part[ob] -= c * Ci[oc]
                     part = alpha[s - 1] * part
                     if i == 0 and s > 1:
                         part = part + beta[s - 1] * B[j][:, off:]
                     acc = part if acc is None else acc + part
                 B[j][:, off:] = acc
         else:
-            for i, (nr, r0) in enumerate(rows):
+            for i, ri in enumerate(R):
                 acc = None
-                for j, (nc, c0) in enumerate(cols):
-                    Aij = A[r0:r0 + nr, c0:c0 + nc]
+                for j, cj in enumerate(Cc):
+                    Aij = A[np.ix_(ri, cj)]
                     Bj = B[j][:, off:]
                     part = Aij @ Bj
-                    lo, hi = max(r0, c0), min(r0 + nr, c0 + nc)
-                    if lo < hi:
-                        part[lo - r0:hi - r0] -= c * Bj[lo - c0:hi - c0]
+                    _, oc, ob = np.intersect1d(ri, cj, return_indices=True)
+                    part[oc] -= c * Bj[ob]
                     part = alpha[s - 1] * part
                     if j == 0:
                         part = part + beta[s - 1] * C[i][:, off:]
                     acc = part if acc is None else acc + part
                 C[i][:, off:] = acc
-    return np.concatenate(C, axis=0)
+    out = np.empty((N, n), dtype=dtype)
+    for i, ri in enumerate(R):
+        out[ri] = C[i]
+    return out

@@ -34,7 +34,8 @@ EXPORTED = (
     "chase_filter_record", "chase_filter_schedule", "chase_cholqr", "chase_cond_est",
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
     "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
-    "chase_set_fused_workspace",
+    "chase_set_fused_workspace", "chase_create_cyclic", "chase_local_indices",
+    "chase_cyclic_indices",
 )
 
 
@@ -77,6 +78,9 @@ def load() -> ctypes.CDLL:
         "chase_get_unique_id": (I32, [ctypes.c_char_p]),
         "chase_create": (I32, [ctypes.POINTER(V), I32, I64, I64, I32, I32, I32, I32, ctypes.c_char_p, I32, V]),
         "chase_set_stream": (I32, [V, V]),
+        "chase_create_cyclic": (I32, [ctypes.POINTER(V), I32, I64, I64, I32, I32, I32, I32, I64, ctypes.c_char_p, I32, V]),
+        "chase_local_indices": (I32, [V, c_i64p, c_i64p]),
+        "chase_cyclic_indices": (I32, [I64, I32, I32, I64, c_i64p, c_i64p]),
         "chase_local_dims": (I32, [V, c_i64p, c_i64p, c_i64p, c_i64p]),
         "chase_block_dims": (I32, [I64, I32, I32, I32, I32, c_i64p, c_i64p, c_i64p, c_i64p]),
         "chase_workspace_size": (I32, [V, ctypes.POINTER(ctypes.c_size_t)]),
@@ -145,11 +149,35 @@ def chase_get_unique_id() -> bytes:
 
 
 def chase_create(dtype: int, N: int, n_max: int, p: int = 1, q: int = 1, myrow: int = 0,
-                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream: int = 0):
+                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream: int = 0,
+                 nb: int = 0):
+    """nb > 0: block-cyclic distribution with block size nb (chase_create_cyclic)."""
     h = ctypes.c_void_p()
-    _check(load().chase_create(ctypes.byref(h), dtype, N, n_max, p, q, myrow, mycol, uid, device,
-                               ctypes.c_void_p(stream)), "chase_create")
+    if nb:
+        _check(load().chase_create_cyclic(ctypes.byref(h), dtype, N, n_max, p, q, myrow, mycol, nb,
+                                          uid, device, ctypes.c_void_p(stream)), "chase_create_cyclic")
+    else:
+        _check(load().chase_create(ctypes.byref(h), dtype, N, n_max, p, q, myrow, mycol, uid, device,
+                                   ctypes.c_void_p(stream)), "chase_create")
     return h
+
+
+def chase_local_indices(h, n_r: int, n_c: int):
+    rows = np.empty(n_r, dtype=np.int64)
+    cols = np.empty(n_c, dtype=np.int64)
+    _check(load().chase_local_indices(h, rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                      cols.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))),
+           "chase_local_indices")
+    return rows, cols
+
+
+def chase_cyclic_indices(N: int, P: int, k: int, nb: int):
+    cnt = ctypes.c_int64()
+    _check(load().chase_cyclic_indices(N, P, k, nb, None, ctypes.byref(cnt)), "chase_cyclic_indices")
+    idx = np.empty(cnt.value, dtype=np.int64)
+    _check(load().chase_cyclic_indices(N, P, k, nb, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                       ctypes.byref(cnt)), "chase_cyclic_indices")
+    return idx
 
 
 def chase_set_stream(h, stream: int):
@@ -309,17 +337,18 @@ class Chase:
     """One handle + its torch-owned workspace (a rank of the p x q grid, one GPU)."""
 
     def __init__(self, dtype: int, N: int, n_max: int, p: int = 1, q: int = 1, myrow: int = 0,
-                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream=None):
+                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream=None, nb: int = 0):
         import torch
         self.device = torch.device("cuda", device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.stream = s
-        self.h = chase_create(dtype, N, n_max, p, q, myrow, mycol, uid, device, s.cuda_stream)
+        self.h = chase_create(dtype, N, n_max, p, q, myrow, mycol, uid, device, s.cuda_stream, nb)
         self.n_r, self.n_c, self.r0, self.c0 = chase_local_dims(self.h)
+        self.rows, self.cols = chase_local_indices(self.h, self.n_r, self.n_c)
         nbytes = chase_workspace_size(self.h)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         chase_set_workspace(self.h, self.ws)
-        self.dtype, self.N, self.n_max, self.p, self.q = dtype, N, n_max, p, q
+        self.dtype, self.N, self.n_max, self.p, self.q, self.nb = dtype, N, n_max, p, q, nb
 
     def filter(self, A_local, V, degrees, c, e, bounds, ncols=None):
         return chase_filter(self.h, A_local, V, degrees, c, e, bounds, ncols)

@@ -86,6 +86,14 @@ static chase_status_t make_map(CUtensorMap* m, const void* base, int64_t rows, i
   return CHASE_OK;
 }
 
+// Block-cyclic distribution with block size nb over P grid rows/columns: grid
+// row k owns global rows g with (g / nb) mod P == k, in increasing order.
+static void cyclic_indices(int64_t N, int P, int k, int64_t nb, std::vector<int64_t>* idx) {
+  idx->clear();
+  for (int64_t b = k; b * nb < N; b += P)
+    for (int64_t g = b * nb; g < std::min(N, (b + 1) * nb); ++g) idx->push_back(g);
+}
+
 static void block_part(int64_t N, int P, int k, int64_t* size, int64_t* start) {
   const int64_t b = N / P, rem = N % P;
   *size = b + (k < rem ? 1 : 0);
@@ -99,7 +107,14 @@ struct chase_handle_s {
   chase_dtype_t dt;
   int64_t N, n_max;
   int p, q, myrow, mycol;
-  int64_t n_r, n_c, r0, c0;
+  int64_t n_r, n_c, r0, c0;       // r0 = c0 = -1 for the block-cyclic distribution
+  int64_t nb = 0;                 // block-cyclic block size (0 = block distribution)
+  std::vector<int64_t> rows_g, cols_g;   // global indices of the local rows / columns
+  int* d_band_odd = nullptr;      // block-cyclic: B-layout row -> C-layout row of the diagonal
+  int* d_band_even = nullptr;     //   C-layout row -> B-layout row of the diagonal (or -1)
+  int* d_b2_src = nullptr;        // residual B2 redistribution: per owning grid row, the source
+  int* d_b2_dst = nullptr;        //   local rows (on the owner) and the B2 rows they fill
+  std::vector<int64_t> b2_seg;    //   segment offsets, p + 1 entries
   int device;
   cudaStream_t stream;
   ncclComm_t world = nullptr, rcomm = nullptr, ccomm = nullptr;
@@ -177,7 +192,7 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, maps, info, s, total;
 };
 // B-layout block (n_c x n_max) | Gram/R (n_max x n_max) | TRSM output W (n_r x n_max)
 // | inverted diagonal blocks of R (64 x n_max) | info | shift
@@ -199,6 +214,8 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)h->n_max * sizeof(double));
   L.nrm = off;
   off += align256((size_t)h->n_max * sizeof(double));
+  L.maps = off;                                         // block-cyclic index maps (int32)
+  off += align256((size_t)(h->n_r + 3 * h->n_c) * sizeof(int));
   L.info = off;
   off += 256;
   L.s = off;
@@ -277,6 +294,7 @@ struct GemmReq {
   double alpha, beta, c;
   int use_beta, band_lo, band_hi, band_shift, upper_only;
   const int* abort_flag;
+  const int* band_map;       // block-cyclic band (device), replaces band_lo/hi/shift
   int a3d;                   // NoTrans: tA is the 3D single-box view (a_d0 multiple of a piece)
   const double* col_shift;   // residual epilogue (Alg.2 l.25): out -= col_shift[n] y2(m, n)
   const void* y2;
@@ -293,6 +311,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
     a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
     a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+    a.band_map = r.band_map;
     a.a3d = r.a3d;
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
@@ -305,6 +324,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
   a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
   a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
+  a.band_map = r.band_map;
   a.a3d = r.a3d;
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
@@ -321,6 +341,7 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
   a.xin = static_cast<const double2*>(r.xin); a.ldx = r.ldx;
   a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
   a.use_beta = 0; a.band_lo = r.band_lo; a.band_hi = r.band_hi; a.band_shift = r.band_shift;
+  a.band_map = r.band_map;
   a.a3d = r.a3d;
   const int grid = std::min(T, h->num_sms);
   if (conj) {
@@ -421,7 +442,19 @@ struct FusedLayout {
 // rows) so a member pushing step s+1 partials never overwrites slots still being summed for s.
 static FusedLayout fused_layout(const chase_handle_s* h) {
   FusedLayout L;
-  const int64_t nr_max = (h->N + h->p - 1) / h->p, nc_max = (h->N + h->q - 1) / h->q;
+  int64_t nr_max = (h->N + h->p - 1) / h->p, nc_max = (h->N + h->q - 1) / h->q;
+  if (h->nb > 0) {                       // block-cyclic: largest local block over the grid
+    std::vector<int64_t> v;
+    nr_max = nc_max = 0;
+    for (int k = 0; k < h->p; ++k) {
+      cyclic_indices(h->N, h->p, k, h->nb, &v);
+      nr_max = std::max<int64_t>(nr_max, (int64_t)v.size());
+    }
+    for (int k = 0; k < h->q; ++k) {
+      cyclic_indices(h->N, h->q, k, h->nb, &v);
+      nc_max = std::max<int64_t>(nc_max, (int64_t)v.size());
+    }
+  }
   const int64_t rows_max = std::max(nr_max, nc_max);
   L.ldc = pad_ld(nr_max);
   L.ldb = pad_ld(nc_max);
@@ -463,6 +496,7 @@ static chase_status_t validate_degrees(int64_t ncols, const int32_t* degrees) {
 struct Geom {
   int64_t n_r, n_c, r0, c0;
   int myrow, mycol;
+  int64_t nb = 0;   // block-cyclic: the band is irregular (device maps); recorded as [-1, -1)
 };
 static void build_schedule(const Geom& gm, int64_t ncols, const int32_t* degrees,
                            std::vector<chase_step_record_t>* rec, int64_t* matvecs) {
@@ -479,7 +513,10 @@ static void build_schedule(const Geom& gm, int64_t ncols, const int32_t* degrees
     r.off = (int32_t)first;
     r.comm = odd ? 0 : 1;
     r.elems = (int64_t)r.k * (odd ? gm.n_c : gm.n_r);
-    if (odd) {   // output rows = B_j rows (global c0 + row); diagonal rows also in [r0, r0+n_r)
+    if (gm.nb > 0) {
+      r.band_lo = r.band_hi = -1;
+      r.use_beta = odd ? ((gm.myrow == 0 && s > 1) ? 1 : 0) : (gm.mycol == 0 ? 1 : 0);
+    } else if (odd) {   // output rows = B_j rows (global c0 + row); diagonal rows also in [r0, r0+n_r)
       r.band_lo = (int32_t)std::max<int64_t>(0, gm.r0 - gm.c0);
       r.band_hi = (int32_t)std::max<int64_t>(r.band_lo, std::min<int64_t>(gm.n_c, gm.r0 + gm.n_r - gm.c0));
       r.use_beta = (gm.myrow == 0 && s > 1) ? 1 : 0;
@@ -532,7 +569,14 @@ chase_status_t chase_block_dims(int64_t N, int p, int q, int i, int j, int64_t* 
 chase_status_t chase_create(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
                             int p, int q, int myrow, int mycol, const uint8_t id[128], int device,
                             void* cuda_stream) {
+  return chase_create_cyclic(out, dt, N, n_max, p, q, myrow, mycol, 0, id, device, cuda_stream);
+}
+
+chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                   int p, int q, int myrow, int mycol, int64_t nb,
+                                   const uint8_t id[128], int device, void* cuda_stream) {
   if (!out) return CHASE_EINVAL;
+  if (nb < 0) return CHASE_EINVAL;
   *out = nullptr;
   if (dt != CHASE_R64 && dt != CHASE_C128) return CHASE_EINVAL;
   if (N < 1 || n_max < 1 || n_max > N || N > (int64_t)INT32_MAX) return CHASE_EINVAL;
@@ -547,8 +591,23 @@ chase_status_t chase_create(chase_handle_t* out, chase_dtype_t dt, int64_t N, in
   h->q = q;
   h->myrow = myrow;
   h->mycol = mycol;
-  block_part(N, p, myrow, &h->n_r, &h->r0);
-  block_part(N, q, mycol, &h->n_c, &h->c0);
+  h->nb = nb;
+  if (nb == 0) {
+    block_part(N, p, myrow, &h->n_r, &h->r0);
+    block_part(N, q, mycol, &h->n_c, &h->c0);
+    for (int64_t l = 0; l < h->n_r; ++l) h->rows_g.push_back(h->r0 + l);
+    for (int64_t l = 0; l < h->n_c; ++l) h->cols_g.push_back(h->c0 + l);
+  } else {
+    cyclic_indices(N, p, myrow, nb, &h->rows_g);
+    cyclic_indices(N, q, mycol, nb, &h->cols_g);
+    h->n_r = (int64_t)h->rows_g.size();
+    h->n_c = (int64_t)h->cols_g.size();
+    h->r0 = h->c0 = -1;
+    if (h->n_r == 0 || h->n_c == 0) {
+      delete h;
+      return CHASE_EINVAL;                    // every grid row/column must own at least one block
+    }
+  }
   h->device = device;
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&h->h_info, sizeof(int)) != cudaSuccess) {
@@ -588,6 +647,23 @@ chase_status_t chase_local_dims(chase_handle_t h, int64_t* n_r, int64_t* n_c, in
   return CHASE_OK;
 }
 
+chase_status_t chase_local_indices(chase_handle_t h, int64_t* rows, int64_t* cols) {
+  if (!h) return CHASE_EINVAL;
+  if (rows) memcpy(rows, h->rows_g.data(), h->rows_g.size() * sizeof(int64_t));
+  if (cols) memcpy(cols, h->cols_g.data(), h->cols_g.size() * sizeof(int64_t));
+  return CHASE_OK;
+}
+
+chase_status_t chase_cyclic_indices(int64_t N, int P, int k, int64_t nb, int64_t* idx,
+                                    int64_t* count) {
+  if (N < 1 || P < 1 || k < 0 || k >= P || nb < 1 || !count) return CHASE_EINVAL;
+  std::vector<int64_t> v;
+  cyclic_indices(N, P, k, nb, &v);
+  *count = (int64_t)v.size();
+  if (idx) memcpy(idx, v.data(), v.size() * sizeof(int64_t));
+  return CHASE_OK;
+}
+
 chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes) {
   if (!h || !bytes) return CHASE_EINVAL;
   *bytes = ws_layout(h).total;
@@ -608,6 +684,39 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->B2ws = base + L.b2;
   h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
   h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
+  if (h->nb > 0) {
+    // block-cyclic maps: band of -cI for both layouts and the residual B2 gather/scatter lists
+    int* maps = reinterpret_cast<int*>(base + L.maps);
+    h->d_band_even = maps;
+    h->d_band_odd = maps + h->n_r;
+    h->d_b2_src = maps + h->n_r + h->n_c;
+    h->d_b2_dst = maps + h->n_r + 2 * h->n_c;
+    std::vector<int> band_even(h->n_r, -1), band_odd(h->n_c, -1), src, dst;
+    std::vector<int64_t> pos_c(h->N, -1), pos_r(h->N, -1);
+    for (int64_t l = 0; l < h->n_c; ++l) pos_c[h->cols_g[l]] = l;
+    for (int64_t l = 0; l < h->n_r; ++l) pos_r[h->rows_g[l]] = l;
+    for (int64_t l = 0; l < h->n_r; ++l) band_even[l] = (int)pos_c[h->rows_g[l]];
+    for (int64_t l = 0; l < h->n_c; ++l) band_odd[l] = (int)pos_r[h->cols_g[l]];
+    h->b2_seg.assign(1, 0);
+    std::vector<int64_t> owner_rows;
+    for (int i2 = 0; i2 < h->p; ++i2) {
+      cyclic_indices(h->N, h->p, i2, h->nb, &owner_rows);
+      std::vector<int64_t> opos(h->N, -1);
+      for (int64_t l = 0; l < (int64_t)owner_rows.size(); ++l) opos[owner_rows[l]] = l;
+      for (int64_t l = 0; l < h->n_c; ++l) {
+        const int64_t g = h->cols_g[l];
+        if (opos[g] >= 0) {
+          src.push_back((int)opos[g]);
+          dst.push_back((int)l);
+        }
+      }
+      h->b2_seg.push_back((int64_t)src.size());
+    }
+    CUDA_TRY(cudaMemcpy(h->d_band_even, band_even.data(), h->n_r * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_band_odd, band_odd.data(), h->n_c * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_b2_src, src.data(), src.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_b2_dst, dst.data(), dst.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
   h->d_info = reinterpret_cast<int*>(base + L.info);
   h->d_shift = reinterpret_cast<double*>(base + L.s);
   return CHASE_OK;
@@ -699,7 +808,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
 
   std::vector<chase_step_record_t> rec;
   int64_t mv;
-  build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol}, ncols, degrees, &rec, &mv);
+  build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol, h->nb}, ncols, degrees, &rec, &mv);
   const int D = (int)rec.size();
 
   // recurrence scalars: alpha_1 = sigma_1/e, beta_1 = 0; alpha_s = 2 sigma_s/e,
@@ -774,6 +883,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.band_lo = r.band_lo;
       g.band_hi = r.band_hi;
       g.band_shift = (int)(h->c0 - h->r0);   // input C row = output B row + c0 - r0
+      g.band_map = h->nb > 0 ? h->d_band_odd : nullptr;
       g.use_beta = r.use_beta;
     } else {
       // C_i = alpha (A_ij B_j - c band(B_j)) + [j == 0] beta C_i
@@ -790,6 +900,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.band_lo = r.band_lo;
       g.band_hi = r.band_hi;
       g.band_shift = (int)(h->r0 - h->c0);   // input B row = output C row + r0 - c0
+      g.band_map = h->nb > 0 ? h->d_band_even : nullptr;
       g.use_beta = r.use_beta;
     }
     const int m = odd ? h->p : h->q;
@@ -1101,6 +1212,37 @@ chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t ld
   if (h->p == 1 && h->q == 1) {
     y2 = V;                                           // C- and B-layout coincide on a 1x1 grid
     ldy2 = ldv;
+  } else if (h->nb > 0) {
+    // block-cyclic: the owner gathers its rows of my column set, Bcast, scatter into B2
+    ProfScope ps(h, CAT_ALLREDUCE, 0);
+    char* stage = static_cast<char*>(h->Wws);
+    for (int i2 = 0; i2 < h->p; ++i2) {
+      const int64_t a = h->b2_seg[i2], cnt = h->b2_seg[i2 + 1] - a;
+      if (cnt == 0) continue;
+      const dim3 grid((unsigned)((cnt + 255) / 256), (unsigned)n);
+      if (h->myrow == i2) {
+        if (h->dt == CHASE_C128)
+          gather_rows_kernel<double2><<<grid, 256, 0, h->stream>>>(
+              reinterpret_cast<const double2*>(V), ldv, h->d_b2_src + a, (int)cnt,
+              reinterpret_cast<double2*>(stage));
+        else
+          gather_rows_kernel<double><<<grid, 256, 0, h->stream>>>(
+              reinterpret_cast<const double*>(V), ldv, h->d_b2_src + a, (int)cnt,
+              reinterpret_cast<double*>(stage));
+        CUDA_TRY(cudaGetLastError());
+      }
+      if (h->p > 1)
+        NCCL_TRY(ncclBroadcast(stage, stage, (size_t)cnt * n * per, ncclDouble, i2, h->ccomm, h->stream));
+      if (h->dt == CHASE_C128)
+        scatter_rows_kernel<double2><<<grid, 256, 0, h->stream>>>(
+            reinterpret_cast<const double2*>(stage), h->d_b2_dst + a, (int)cnt,
+            reinterpret_cast<double2*>(B2), ldb);
+      else
+        scatter_rows_kernel<double><<<grid, 256, 0, h->stream>>>(
+            reinterpret_cast<const double*>(stage), h->d_b2_dst + a, (int)cnt,
+            reinterpret_cast<double*>(B2), ldb);
+      CUDA_TRY(cudaGetLastError());
+    }
   } else {
     ProfScope ps(h, CAT_ALLREDUCE, 0);
     char* stage = static_cast<char*>(h->Wws);

@@ -51,6 +51,7 @@ struct DGemmArgs {
   int band_shift;
   int upper_only;
   const int* abort_flag;
+  const int* band_map;     // non-null (block-cyclic): see zgemm.cuh
   int a3d;                 // NoTrans only: tmA is the 3D view {16 doubles, k, m/16} -> 1 TMA/stage
   const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (Alg.2 l.25)
   const double* y2;
@@ -202,8 +203,9 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
         if (row < g.M && col < g.N) {
           double v = acc[mt][nt][r];
-          if (row >= g.band_lo && row < g.band_hi)
-            v -= g.c * g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+          const int bsrc = g.band_map != nullptr ? g.band_map[row]
+                           : (row >= g.band_lo && row < g.band_hi ? row + g.band_shift : -1);
+          if (bsrc >= 0) v -= g.c * g.xin[(long long)bsrc + (long long)col * g.ldx];
           if (g.col_shift != nullptr) v -= g.col_shift[col] * g.y2[(long long)row + (long long)col * g.ldy2];
           v *= g.alpha;
           double* o = g.out + (long long)row + (long long)col * g.ldo;

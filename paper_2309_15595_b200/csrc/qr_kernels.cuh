@@ -168,6 +168,21 @@ __global__ void colnorm2_kernel(const T* B, long long ld, int rows, double* nrm)
   if (tid == 0) nrm[col] = part[0];
 }
 
+// Block-cyclic B2 redistribution (Alg.2 l.23 on a cyclic grid): gather local rows idx[0..cnt)
+// of V into a dense cnt x ncols stage (ld cnt), and scatter a stage into rows idx of B2.
+template <typename T>
+__global__ void gather_rows_kernel(const T* V, long long ldv, const int* idx, int cnt, T* stage) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long col = blockIdx.y;
+  if (i < cnt) stage[(long long)i + col * cnt] = V[(long long)idx[i] + col * ldv];
+}
+template <typename T>
+__global__ void scatter_rows_kernel(const T* stage, const int* idx, int cnt, T* B2, long long ldb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long col = blockIdx.y;
+  if (i < cnt) B2[(long long)idx[i] + col * ldb] = stage[(long long)i + col * cnt];
+}
+
 // Alg.2 l.28 "resd <- sqrt(nrm)" on the reduced squared norms.
 __global__ void sqrt_kernel(double* v, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -67,6 +67,8 @@ struct ZGemmArgs {
   int band_shift;
   int upper_only;          // skip CTAs whose tile lies strictly below the diagonal (m > n)
   const int* abort_flag;   // non-null: skip the whole GEMM when *abort_flag != 0 (POTRF info)
+  const int* band_map;     // non-null (block-cyclic): out row m subtracts c * xin[band_map[m], n]
+                           //   when band_map[m] >= 0; replaces [band_lo, band_hi)
   int a3d;                 // NoTrans only: tmA is the 3D view {8 complex, k, m/8} -> 1 TMA/stage
   const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (residual,
   const double2* y2;       //   Alg.2 l.25 "B <- B - ritzv B2" fused into the HEMM epilogue)
@@ -261,8 +263,10 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
         if (row < g.M && col < g.N) {
           double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
-          if (row >= g.band_lo && row < g.band_hi) {
-            const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+          const int bsrc = g.band_map != nullptr ? g.band_map[row]
+                           : (row >= g.band_lo && row < g.band_hi ? row + g.band_shift : -1);
+          if (bsrc >= 0) {
+            const double2 x = g.xin[(long long)bsrc + (long long)col * g.ldx];
             vr -= g.c * x.x;
             vi -= g.c * x.y;
           }

@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
           if (row < g.M && col < g.N) {
             double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
-            if (row >= g.band_lo && row < g.band_hi) {
-              const double2 x = g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+            const int bsrc = g.band_map != nullptr ? g.band_map[row]
+                             : (row >= g.band_lo && row < g.band_hi ? row + g.band_shift : -1);
+            if (bsrc >= 0) {
+              const double2 x = g.xin[(long long)bsrc + (long long)col * g.ldx];
               vr -= g.c * x.x;
               vi -= g.c * x.y;
             }

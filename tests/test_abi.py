@@ -96,3 +96,14 @@ def test_cond_est_matches_oracle(seed):
 def test_shift_value_golden(golden):
     g = golden["shift"]
     assert cb.chase_shift_value(g["m"], g["n"], g["norm"]) == g["s_over_u"] * 2.0 ** -53
+
+
+@pytest.mark.parametrize("N,P,nb", [(10, 2, 4), (61, 3, 1), (301, 4, 7), (1000, 2, 64)])
+def test_cyclic_indices_partition(N, P, nb):
+    """chase_cyclic_indices: grid rows partition 0..N-1, blocks of nb dealt round-robin."""
+    seen = np.concatenate([cb.chase_cyclic_indices(N, P, k, nb) for k in range(P)])
+    assert np.array_equal(np.sort(seen), np.arange(N))
+    for k in range(P):
+        idx = cb.chase_cyclic_indices(N, P, k, nb)
+        assert np.all((idx // nb) % P == k) and np.all(np.diff(idx) > 0)
+        assert np.array_equal(idx, ci.cyclic_indices(N, P, k, nb))

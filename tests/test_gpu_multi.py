@@ -44,19 +44,25 @@ def torchrun(nproc, script_args, timeout):
 GRIDS = [(2, 1), (1, 2), (2, 2), (4, 1), (1, 4)]
 
 
-@pytest.mark.parametrize("complex_,grid,pad,mode", [(c, g, 0, "nccl") for c in (True, False) for g in GRIDS] +
-                         [(True, (1, 2), 6, "nccl"), (False, (1, 2), 5, "nccl"), (True, (2, 2), 6, "nccl")] +
-                         [(True, g, 0, "fused") for g in GRIDS] + [(True, (1, 2), 6, "fused")])
-def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode):
+CASES = ([(c, g, 0, "nccl", 0) for c in (True, False) for g in GRIDS] +
+         [(True, (1, 2), 6, "nccl", 0), (False, (1, 2), 5, "nccl", 0), (True, (2, 2), 6, "nccl", 0)] +
+         [(True, g, 0, "fused", 0) for g in GRIDS] + [(True, (1, 2), 6, "fused", 0)] +
+         [(True, (2, 1), 0, "nccl", 7), (False, (1, 2), 0, "nccl", 1), (True, (2, 2), 0, "nccl", 16),
+          (True, (1, 2), 0, "fused", 5), (True, (2, 2), 0, "fused", 32), (False, (2, 2), 0, "nccl", 3)])
+
+
+@pytest.mark.parametrize("complex_,grid,pad,mode,nb", CASES)
+def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode, nb):
     """pad > 0: leading dimensions larger than the local rows (strided AllReduce path).
-    mode "fused": filter steps as one HEMM + NVLink peer-memory reduction kernel."""
+    mode "fused": filter steps as one HEMM + NVLink peer-memory reduction kernel.
+    nb > 0: block-cyclic distribution with block size nb."""
     p, q = grid
     if ngpus() < p * q:
         pytest.skip(f"needs {p * q} GPUs")
     N = 301
     out = str(tmp_path / "res.npz")
     r = torchrun(p * q, [os.path.join(ROOT, "tests", "mp_gpu_worker.py"), str(p), str(q), str(N),
-                         "c" if complex_ else "r", out, str(pad), mode], 600)
+                         "c" if complex_ else "r", out, str(pad), mode, str(nb)], 600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = np.load(out)
     degs = sorted([2, 2, 4, 4, 4, 6, 8, 8, 10, 10, 12, 12, 12, 14, 16, 18, 20] * 3)
@@ -72,9 +78,13 @@ def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode):
     assert float(res["replica"]) == 0.0                       # identical bits on all replicas
     assert np.all(res["repeat_equal"])                        # bitwise repeatable
     assert np.all(res["mv"] == sum(degs))
-    for (i, j, nr), recs in zip(res["ranks"], res["recs"]):
-        n_r, n_c, _, _ = ci.block_dims(N, p, q, int(i), int(j))
-        orec, _ = oracle.filter_record(degs, n_r, n_c)
+    for (i, j, n_r, n_c), recs in zip(res["ranks"], res["recs"]):
+        if nb == 0:
+            assert (n_r, n_c) == ci.block_dims(N, p, q, int(i), int(j))[:2]
+        else:
+            assert n_r == len(ci.cyclic_indices(N, p, int(i), nb))
+            assert n_c == len(ci.cyclic_indices(N, q, int(j), nb))
+        orec, _ = oracle.filter_record(degs, int(n_r), int(n_c))
         assert recs == str(orec)
     qref = oracle.caqr(ref, float(res["est"]))
     assert np.all(res["status"] == 0)

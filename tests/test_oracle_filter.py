@@ -166,3 +166,18 @@ def test_grid_scheme_equals_global(grid):
     ref, _ = oracle.chebyshev_filter(A, V, degs, b.c, b.e, b.mu_1)
     got = oracle.distributed_filter(A, V, degs, b.c, b.e, b.mu_1, *grid)
     assert relF(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("grid,nb", [((2, 1), 1), ((1, 2), 3), ((2, 2), 4), ((2, 3), 5), ((3, 2), 16)])
+def test_block_cyclic_scheme_equals_global(grid, nb):
+    """Block-cyclic distribution: same recurrence, diagonal share = rows owned in
+    both index sets."""
+    N = 61
+    lam = ci.uniform_spectrum(N)
+    A = ci.dense_from_spectrum(lam, 43, True)
+    degs = [2, 4, 4, 8, 12, 20]
+    V = ci.gaussian_block(N, len(degs), 44, True)
+    b = ci.bounds_from_spectrum(lam, len(degs))
+    ref, _ = oracle.chebyshev_filter(A, V, degs, b.c, b.e, b.mu_1)
+    got = oracle.distributed_filter(A, V, degs, b.c, b.e, b.mu_1, *grid, nb=nb)
+    assert relF(got, ref) <= 1e-13
