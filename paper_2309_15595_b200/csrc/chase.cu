@@ -137,6 +137,7 @@ struct chase_handle_s {
   int world_size = 1;
   unsigned fused_ep = 0;
   unsigned long long fused_delivered = 0;
+  unsigned long long fused_ctr = 0;          // tile-scheduler counter value at the next launch
   int* d_err = nullptr;
   int num_sms = 148;
   // bookkeeping of the last filter call
@@ -435,7 +436,7 @@ static chase_status_t allreduce_cols(chase_handle_s* h, void* buf, int64_t rows,
 //   done  u64 delivery counter, err i32
 struct FusedLayout {
   int64_t ldc, ldb, ldpo, ldpe;
-  size_t cw, bw, po, pe, flags, done, err, total;
+  size_t cw, bw, po, pe, flags, done, err, ctr, total;
   int64_t tiles_max;
 };
 // Staging areas by step parity (odd steps: p slots of B-layout rows, even: q slots of C-layout
@@ -475,6 +476,8 @@ static FusedLayout fused_layout(const chase_handle_s* h) {
   L.done = off;
   off += 256;
   L.err = off;
+  off += 256;
+  L.ctr = off;                                          // dynamic tile-scheduler counter
   off += 256;
   L.total = off;
   return L;
@@ -752,6 +755,7 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
   h->d_err = reinterpret_cast<int*>(static_cast<char*>(local) + L.err);
   h->fused_ep = 0;
   h->fused_delivered = 0;
+  h->fused_ctr = 0;
   h->fused = true;
   return CHASE_OK;
 }
@@ -926,8 +930,12 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       f.err = h->d_err;
       static const bool plain = getenv("CHASE_FUSED_PLAIN") != nullptr;
       f.plain = (m == 1 && plain) ? 1 : 0;
+      f.tile_ctr = reinterpret_cast<unsigned long long*>(h->fz_base[me_world] + FL.ctr);
+      f.ctr_base = h->fused_ctr;
       g.use_beta = 0;                        // the tile owner adds beta * old after the sum
       const int T = ((g.M + ZG_BM - 1) / ZG_BM) * ((g.N + ZG_BN - 1) / ZG_BN);
+      // every CTA grabs until it sees an index >= T: T + grid increments per launch
+      h->fused_ctr += (unsigned long long)T + (unsigned long long)std::min(T, h->num_sms);
       ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
       STATUS_TRY(launch_zgemm_fused(h, g.conj, *g.tA, *g.tX, g, f, T));
       h->fused_delivered += (unsigned long long)T;

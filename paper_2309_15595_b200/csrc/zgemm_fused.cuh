@@ -41,6 +41,8 @@ struct FusedArgs {
   int owner_beta;                            // owner adds beta * out(old) before broadcasting
   int* err;                                  // set on a spin timeout
   int plain;                                 // diagnostics: local epilogue, no protocol (m == 1)
+  unsigned long long* tile_ctr;              // dynamic tile scheduler (monotonic, local)
+  unsigned long long ctr_base;               // value of *tile_ctr when this launch starts
 };
 
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
@@ -71,10 +73,16 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   const int T = n_tiles * m_tiles;
-  const int my_tiles = (T - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
-  const int L = my_tiles * KT;                        // k-tiles this CTA streams
-  auto tile_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
+  // dynamic tile scheduler: the producer grabs the next tile from a global counter and passes it
+  // to the MMA warps through a small smem ring (tile -1 = no more tiles)
+  constexpr int RING = ZG_STAGES + 2;
+  __shared__ int s_tile[RING];
+  int issued = 0;                                      // k-tiles with TMA in flight (thread 0)
+  auto grab = [&]() -> int {
+    const unsigned long long v = atomicAdd(f.tile_ctr, 1ull) - f.ctr_base;
+    return v < (unsigned long long)T ? (int)v : -1;
+  };
   auto tile_origin = [&](int t, int& m0, int& n0) {  // grouped rasterisation as in zgemm
     const int group = t / (ZG_GROUP_M * n_tiles);
     const int first_m = group * ZG_GROUP_M;
@@ -104,13 +112,25 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  if (s_abort || L == 0) return;
+  if (s_abort) return;
 
-  // k-tile stream: issue() is called by thread 0 for gs = 0, 1, 2, ... in order, so the
-  // (tile, kt, m0, n0) of the next load are advanced incrementally (no per-k-tile division)
+  // k-tile stream: issue() is called by thread 0 for gs = 0, 1, 2, ... in order; (tile, kt, m0,
+  // n0) of the next load advance incrementally.  When the scheduler runs dry the stage gets a
+  // plain arrive (no bytes) and its ring entry says -1.
   int is_seq = 0, is_kt = 0, is_m0 = 0, is_n0 = 0;
-  if (threadIdx.x == 0) tile_origin(tile_of(0), is_m0, is_n0);
+  bool prod_done = false;
   auto issue = [&](int s) {
+    if (prod_done) return;
+    if (is_kt == 0) {
+      const int t = grab();
+      s_tile[is_seq % RING] = t;
+      if (t < 0) {
+        prod_done = true;
+        mbar_arrive(&full[s]);
+        return;
+      }
+      tile_origin(t, is_m0, is_n0);
+    }
     const int kt = is_kt, m0 = is_m0, n0 = is_n0;
     mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
     uint8_t* sa = smem + s * ZG_STAGE_BYTES;
@@ -130,15 +150,16 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       }
       tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
+    ++issued;
     if (++is_kt == KT) {
       is_kt = 0;
-      if (++is_seq < my_tiles) tile_origin(tile_of(is_seq), is_m0, is_n0);
+      ++is_seq;
     }
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmX);
-    for (int gs = 0; gs < ZG_STAGES && gs < L; ++gs) issue(gs);
+    for (int gs = 0; gs < ZG_STAGES; ++gs) issue(gs);
   }
 
   const int wm = warp & 3, wn = warp >> 2;
@@ -320,10 +341,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   Frag cur, nxt;
   mbar_wait(&full[0], 0);
+  int tile = s_tile[0];
+  if (tile < 0) return;
   load(cur, 0, 0, 0);
-  int kt = 0;                                          // k-tile of gs inside its output tile
-  for (int gs = 0; gs < L; ++gs) {
+  int seq = 0, kt = 0, gs = 0;
+  for (;;) {
     const int s = gs % ZG_STAGES;
+    int next_tile = tile;
 #pragma unroll
     for (int sub = 0; sub < SUBS; ++sub) {
       if (sub + 1 < SUBS) {
@@ -331,31 +355,36 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (gs + 1 < L) {
-          mbar_wait(&full[(gs + 1) % ZG_STAGES], ((gs + 1) / ZG_STAGES) & 1);
-          load(nxt, gs + 1, kt + 1 == KT ? 0 : kt + 1, 0);
+        mbar_wait(&full[(gs + 1) % ZG_STAGES], ((gs + 1) / ZG_STAGES) & 1);
+        if (kt + 1 < KT) {
+          load(nxt, gs + 1, kt + 1, 0);
+        } else {
+          next_tile = s_tile[(seq + 1) % RING];
+          if (next_tile >= 0) load(nxt, gs + 1, 0, 0);
         }
       }
       mma(cur);
       cur = nxt;
     }
-    if (threadIdx.x == 0 && gs >= 1 && gs - 1 + ZG_STAGES < L) {
+    if (threadIdx.x == 0 && gs >= 1) {
       const int sp = (gs - 1) % ZG_STAGES;
-      mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
+      if (!prod_done) mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
       issue(sp);
     }
-    if (kt == KT - 1) {
-      epilogue(tile_of(gs / KT));
-      kt = -1;
+    ++gs;
+    if (++kt == KT) {
+      epilogue(tile);
       zero_acc();
-      if (s_abort) {
-        // drain: the TMA loads already issued must land before the CTA exits
-        for (int r = gs + 1; r < L && r < gs + ZG_STAGES; ++r)
-          mbar_wait(&full[r % ZG_STAGES], (r / ZG_STAGES) & 1);
+      if (s_abort) {              // a peer never arrived: give up (the host reports CHASE_ECUDA)
+        if (threadIdx.x == 0)     // let the loads already in flight land before the CTA exits
+          for (int r = gs; r < issued; ++r) mbar_wait(&full[r % ZG_STAGES], (r / ZG_STAGES) & 1);
         return;
       }
+      kt = 0;
+      ++seq;
+      tile = next_tile;
+      if (tile < 0) break;
     }
-    ++kt;
   }
 }
 
