@@ -217,7 +217,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-cols", type=int, default=2)
-    ap.add_argument("--comm", default="nccl", choices=["fused", "nccl"],
+    ap.add_argument("--comm", default="fused", choices=["fused", "nccl"],
                     help="N > 1: filter steps as fused HEMM + NVLink reduction kernels, or HEMM + ncclAllReduce")
     args = ap.parse_args()
     if args.impl == "reference":
