@@ -11,6 +11,8 @@ Workloads (BASELINE.json configs, synthetic, seeded):
     N=2  weak-scaling point of C2 (paper Fig.3a recipe, N ~ 30000 sqrt(P)): N=42432, n=3000, 2x1
     N=4  N=60000, n=3000, 2x2
     N=8  C4: N=120000 complex Uniform, nev=1200 nex=400, degree 20, 2x4 (north-star target)
+N > 1 filter steps run as fused HEMM + NVLink peer-memory reduction kernels (--comm fused,
+default for complex workloads) or as HEMM + ncclAllReduce (--comm nccl).
 Metric (BASELINE.json): Chebyshev filter FP64 TFLOP/s (max over ranks): algorithmic filter
 flops 8 N^2 sum_j d_j (complex; 2 N^2 sum d real) divided by the whole step time (filter +
 QR), so QR time is charged against the filter number (conservative).
@@ -264,8 +266,11 @@ def main():
         comm_mode = "nccl"
         if args.comm == "fused" and w["complex_"]:
             from paper_2309_15595_b200 import dist as cdist
-            cdist.enable_fused_comm(h)
-            comm_mode = "fused HEMM + NVLink peer-memory reduction"
+            try:
+                cdist.enable_fused_comm(h)
+                comm_mode = "fused HEMM + NVLink peer-memory reduction"
+            except Exception as exc:      # e.g. no peer mapping on this box: stay on NCCL
+                comm_mode = f"nccl (fused unavailable: {type(exc).__name__})"
 
     # ---- inputs, resident in HBM before the timed region
     gen = generator(w, lam)
