@@ -996,7 +996,7 @@ void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n
   potrf_diag_kernel<T><<<1, 256, diag_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info);
   h->launches[CAT_POTRF]++;
   if (rest > 0) {
-    potrf_panel_kernel<T><<<(rest + PANEL_THREADS - 1) / PANEL_THREADS, PANEL_THREADS,
+    potrf_panel_kernel<T><<<(rest + PANEL_THREADS - 1) / PANEL_THREADS, PANEL_BLOCK,
                             panel_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, n,
                                                           h->d_info);
     h->launches[CAT_POTRF]++;

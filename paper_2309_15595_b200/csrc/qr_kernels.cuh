@@ -27,6 +27,8 @@ __device__ __forceinline__ double2 s_cmul(double2 a, double2 b) {  // conj(a) * 
 }
 __device__ __forceinline__ double s_cmul(double a, double b) { return a * b; }
 __device__ __forceinline__ double2 s_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 s_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double s_add(double a, double b) { return a + b; }
 __device__ __forceinline__ double s_sub(double a, double b) { return a - b; }
 __device__ __forceinline__ double2 s_div(double2 a, double r) { return make_double2(a.x / r, a.y / r); }
 __device__ __forceinline__ double s_div(double a, double r) { return a / r; }
@@ -49,12 +51,14 @@ __global__ void potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info)
   extern __shared__ __align__(16) unsigned char qr_dyn[];
   T (*S)[QR_NB + 1] = reinterpret_cast<T (*)[QR_NB + 1]>(qr_dyn);   // S[a][b] = G[kb+a, kb+b]
   if (*info != 0) return;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int idx = tid; idx < nb * nb; idx += nt) {
-    const int a = idx % nb, b = idx / nb;
-    S[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
+  // 256 threads: thread (ty, b) owns column b = tid % 64 and rows ty, ty+4, ... of it
+  const int tid = threadIdx.x, b = tid & (QR_NB - 1), ty = tid >> 6;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {   // coalesced: rows fastest
+    const int a = idx % nb, c = idx / nb;
+    S[a][c] = G[(long long)(kb + a) + (long long)(kb + c) * ld];
   }
   __syncthreads();
+  double rdiag = 0.0;                       // R[b][b], kept by the threads of column b
   for (int j = 0; j < nb; ++j) {
     const double d = s_re(S[j][j]);
     if (!(d > 0.0)) {                       // uniform: every thread reads the same d
@@ -62,53 +66,72 @@ __global__ void potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info)
       return;
     }
     const double r = sqrt(d);
-    __syncthreads();
-    for (int l = j + 1 + tid; l < nb; l += nt) S[j][l] = s_div(S[j][l], r);
-    if (tid == 0) S[j][j] = s_real<T>(r);
+    if (b == j) rdiag = r;
+    if (ty == 0 && b > j && b < nb) S[j][b] = s_div(S[j][b], r);   // row j of R
     __syncthreads();
     // trailing update of the upper triangle: S[a][b] -= conj(R[j][a]) R[j][b], j < a <= b
-    const int w = nb - j - 1;
-    for (int idx = tid; idx < w * w; idx += nt) {
-      const int a = j + 1 + idx % w, b = j + 1 + idx / w;
-      if (a <= b) S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], S[j][b]));
+    if (b > j && b < nb) {
+      const T rjb = S[j][b];
+      for (int a = j + 1 + ty; a <= b; a += 4) S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], rjb));
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < nb * nb; idx += nt) {
-    const int a = idx % nb, b = idx / nb;
-    if (a <= b) G[(long long)(kb + a) + (long long)(kb + b) * ld] = S[a][b];
+  if (ty == 0 && b < nb) S[b][b] = s_real<T>(rdiag);
+  __syncthreads();
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {   // coalesced store of the upper part
+    const int a = idx % nb, c = idx / nb;
+    if (a <= c) G[(long long)(kb + a) + (long long)(kb + c) * ld] = S[a][c];
   }
 }
 
 // R_kk^H Y = G[kb:kb+nb, kb+nb:n]: one thread per column, R_kk broadcast from smem, the column
 // kept in smem laid out [row][thread] (conflict free).
-constexpr int PANEL_THREADS = 128;
+constexpr int PANEL_THREADS = 64;    // columns per CTA (one solving thread each)
+constexpr int PANEL_BLOCK = 256;     // threads per CTA for the coalesced loads/stores
 template <typename T>
 constexpr int panel_smem() { return (QR_NB * QR_NB + QR_NB * PANEL_THREADS) * (int)sizeof(T); }
 template <typename T>
-__global__ void __launch_bounds__(PANEL_THREADS)
+__global__ void __launch_bounds__(PANEL_BLOCK)
     potrf_panel_kernel(T* G, long long ld, int kb, int nb, int n, const int* info) {
   extern __shared__ __align__(16) unsigned char qr_dyn[];
   T (*R)[QR_NB] = reinterpret_cast<T (*)[QR_NB]>(qr_dyn);
   T (*Y)[PANEL_THREADS] = reinterpret_cast<T (*)[PANEL_THREADS]>(qr_dyn + QR_NB * QR_NB * sizeof(T));
   if (*info != 0) return;
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < nb * nb; idx += PANEL_THREADS) {
+  for (int idx = tid; idx < nb * nb; idx += PANEL_BLOCK) {
     const int a = idx % nb, b = idx / nb;
     R[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
   }
-  const int col = kb + nb + blockIdx.x * PANEL_THREADS + tid;
+  const int col0 = kb + nb + blockIdx.x * PANEL_THREADS;
+  const int col = col0 + tid;
   const bool active = col < n;
-  if (active)
-    for (int a = 0; a < nb; ++a) Y[a][tid] = G[(long long)(kb + a) + (long long)col * ld];
+  // coalesced load of the nb x PANEL_THREADS panel by all PANEL_BLOCK threads (rows fastest)
+  for (int idx = tid; idx < nb * PANEL_THREADS; idx += PANEL_BLOCK) {
+    const int a = idx % nb, c = idx / nb;
+    if (col0 + c < n) Y[a][c] = G[(long long)(kb + a) + (long long)(col0 + c) * ld];
+  }
   __syncthreads();
-  if (!active) return;
+  if (tid < PANEL_THREADS) {
   for (int a = 0; a < nb; ++a) {
-    T acc = Y[a][tid];
-    for (int b = 0; b < a; ++b) acc = s_sub(acc, s_cmul(R[b][a], Y[b][tid]));  // (R^H)[a][b]
+    // (R^H)[a][b] = conj(R[b][a]); four partial sums break the dependency chain
+    T acc0 = Y[a][tid], acc1 = s_real<T>(0.0), acc2 = s_real<T>(0.0), acc3 = s_real<T>(0.0);
+    int b = 0;
+    for (; b + 3 < a; b += 4) {
+      acc0 = s_sub(acc0, s_cmul(R[b][a], Y[b][tid]));
+      acc1 = s_sub(acc1, s_cmul(R[b + 1][a], Y[b + 1][tid]));
+      acc2 = s_sub(acc2, s_cmul(R[b + 2][a], Y[b + 2][tid]));
+      acc3 = s_sub(acc3, s_cmul(R[b + 3][a], Y[b + 3][tid]));
+    }
+    for (; b < a; ++b) acc0 = s_sub(acc0, s_cmul(R[b][a], Y[b][tid]));
+    T acc = s_add(s_add(acc0, acc1), s_add(acc2, acc3));
     acc = s_div(acc, s_re(R[a][a]));
-    Y[a][tid] = acc;
-    G[(long long)(kb + a) + (long long)col * ld] = acc;
+    if (active) Y[a][tid] = acc;
+  }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nb * PANEL_THREADS; idx += PANEL_BLOCK) {
+    const int a = idx % nb, c = idx / nb;
+    if (col0 + c < n) G[(long long)(kb + a) + (long long)(col0 + c) * ld] = Y[a][c];
   }
 }
 
@@ -139,9 +162,14 @@ __global__ void __launch_bounds__(TRTRI_NB)
   if (j < nb) {
     X[j][j] = s_real<T>(1.0 / s_re(R[j][j]));
     for (int i = j - 1; i >= 0; --i) {
-      T acc = s_real<T>(0.0);
-      for (int l = i + 1; l <= j; ++l) acc = s_sub(acc, s_mul(R[i][l], X[l][j]));
-      X[i][j] = s_div(acc, s_re(R[i][i]));
+      T a0 = s_real<T>(0.0), a1 = s_real<T>(0.0);
+      int l = i + 1;
+      for (; l + 1 <= j; l += 2) {
+        a0 = s_sub(a0, s_mul(R[i][l], X[l][j]));
+        a1 = s_sub(a1, s_mul(R[i][l + 1], X[l + 1][j]));
+      }
+      if (l <= j) a0 = s_sub(a0, s_mul(R[i][l], X[l][j]));
+      X[i][j] = s_div(s_add(a0, a1), s_re(R[i][i]));
     }
   }
   for (int i = 0; i < TRTRI_NB; ++i) Rinv[(long long)i + (long long)(kb + j) * TRTRI_NB] = X[i][j];
