@@ -237,6 +237,19 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
                             chase_stats_t* stats, int32_t* info);
 
 /* ---------------------------------------------------------------------------------------
+ * Rayleigh-Ritz -- Alg.2 l.16-22 on the orthonormal
+ * C-layout block V (ncols columns, e.g. the chase_cholqr output):
+ *   B2 <- Bcast(C2, ccomm); B <- H C (odd-step HEMM), AllReduce(ccomm);
+ *   A <- B2^H B, AllReduce(rcomm);  Lambda, Y <- HEEVD(A)  (own GPU parallel block-Jacobi
+ *   eigensolver, redundant and bit-identical on every rank);  V <- V Y.
+ *  ritz    host out: the ncols Ritz values, ascending (V's columns in the same order).
+ *  sweeps  host out, nullable: Jacobi sweeps used (convergence: off(A) <= 1e-14 ||A||_F).
+ * Uses the B-layout, Gram and eigensolver workspace.  Synchronises the stream once per sweep.
+ * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL. */
+chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_t lda, void* V,
+                                   int64_t ldv, int64_t ncols, double* ritz, int32_t* sweeps);
+
+/* ---------------------------------------------------------------------------------------
  * Residuals -- Alg.2 l.23-28: resid[j] = ||H v_j - ritz[j] v_j||_2
  * for the ncols columns of V (Ritz vectors, C-layout):
  *   B2 <- Bcast(C, ccomm) (rows [c0, c0+n_c) of V, from the owning rank(s) of the column

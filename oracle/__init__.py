@@ -20,3 +20,4 @@ from .qr import (gram, potrf_upper, trsm_right_upper, shift_value, cholesky_qr, 
                  cond_est, select_variant, householder_qr, frobenius_sq)
 from .grid import distributed_filter  # noqa: F401
 from .residual import residuals  # noqa: F401
+from .rayleigh_ritz import rayleigh_ritz  # noqa: F401

@@ -35,7 +35,7 @@ EXPORTED = (
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
     "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
     "chase_set_fused_workspace", "chase_create_cyclic", "chase_local_indices",
-    "chase_cyclic_indices",
+    "chase_cyclic_indices", "chase_rayleigh_ritz",
 )
 
 
@@ -94,6 +94,7 @@ def load() -> ctypes.CDLL:
         "chase_cond_est": (D, [ctypes.POINTER(D), I64, D, D, ctypes.POINTER(I32), I64]),
         "chase_residuals": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "chase_fused_workspace_size": (I32, [V, ctypes.POINTER(ctypes.c_size_t)]),
+        "chase_rayleigh_ritz": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(I32)]),
         "chase_set_fused_workspace": (I32, [V, V, ctypes.POINTER(ctypes.c_uint64), I32]),
         "chase_shift_value": (D, [I64, I64, D]),
         "chase_profile_enable": (I32, [V, I32]),
@@ -294,6 +295,19 @@ def chase_residuals(h, A_local, V, ritz, ncols: int | None = None):
     return out
 
 
+def chase_rayleigh_ritz(h, A_local, V, ncols: int | None = None):
+    """Rayleigh-Ritz (Alg.2 l.16-22) in place on V; returns (ritz values ascending, sweeps)."""
+    a_ptr, lda = _colmajor(A_local, "A_local")
+    v_ptr, ldv = _colmajor(V, "V")
+    ncols = V.shape[1] if ncols is None else ncols
+    out = np.empty(ncols, dtype=np.float64)
+    sw = ctypes.c_int32()
+    _check(load().chase_rayleigh_ritz(h, a_ptr, lda, v_ptr, ldv, ncols,
+                                      out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                      ctypes.byref(sw)), "chase_rayleigh_ritz")
+    return out, sw.value
+
+
 def chase_cond_est(ritz, c: float, e: float, degrees, locked: int = 0) -> float:
     """Alg.5 over the n = len(degrees) vectors; ritz needs at least n values (ascending)."""
     r = np.ascontiguousarray(np.asarray(ritz, dtype=np.float64))
@@ -355,6 +369,9 @@ class Chase:
 
     def cholqr(self, V, cond_est, ncols=None, raise_on_error=True):
         return chase_cholqr(self.h, V, cond_est, ncols, raise_on_error)
+
+    def rayleigh_ritz(self, A_local, V, ncols=None):
+        return chase_rayleigh_ritz(self.h, A_local, V, ncols)
 
     def residuals(self, A_local, V, ritz, ncols=None):
         return chase_residuals(self.h, A_local, V, ritz, ncols)

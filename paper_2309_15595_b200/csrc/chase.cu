@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +15,7 @@
 
 #include "chase.h"
 #include "dgemm.cuh"
+#include "eig.cuh"
 #include "qr_kernels.cuh"
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
@@ -126,6 +128,7 @@ struct chase_handle_s {
   void* Wws = nullptr;      // n_r x n_max (TRSM output)
   void* Rinv = nullptr;     // 64 x n_max (inverted diagonal blocks of R)
   void* B2ws = nullptr;     // n_c x n_max (C redistributed into B-layout, Alg.2 l.23)
+  char* eigws = nullptr;    // Jacobi eigensolver region (see eig_bytes)
   double* d_ritz = nullptr;
   double* d_nrm = nullptr;
   int* d_info = nullptr;
@@ -193,8 +196,17 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, maps, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, info, s, total;
 };
+// Jacobi eigensolver buffers (Rayleigh-Ritz): A ping-pong, Y ping-pong, U_bd (np x np complex
+// each, np = n_max rounded up to 64) + eigenvalues, order, permutation tables, partial sums.
+static int64_t eig_np(int64_t n) { return (n + JAC_PW - 1) / JAC_PW * JAC_PW; }
+static size_t eig_bytes(int64_t n_max) {
+  const int64_t np = eig_np(n_max), L = np / 32;
+  return 5 * align256((size_t)np * np * 16) + align256(np * sizeof(double)) +
+         align256(np * sizeof(int)) + align256((size_t)(L + 1) * L * sizeof(int)) +
+         align256(2 * JAC_RED_BLOCKS * sizeof(double) + 2 * sizeof(double));
+}
 // B-layout block (n_c x n_max) | Gram/R (n_max x n_max) | TRSM output W (n_r x n_max)
 // | inverted diagonal blocks of R (64 x n_max) | info | shift
 static WsLayout ws_layout(const chase_handle_s* h) {
@@ -217,6 +229,8 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)h->n_max * sizeof(double));
   L.maps = off;                                         // block-cyclic index maps (int32)
   off += align256((size_t)(h->n_r + 3 * h->n_c) * sizeof(int));
+  L.eig = off;                                          // Rayleigh-Ritz eigensolver
+  off += eig_bytes(h->n_max);
   L.info = off;
   off += 256;
   L.s = off;
@@ -296,6 +310,7 @@ struct GemmReq {
   int use_beta, band_lo, band_hi, band_shift, upper_only;
   const int* abort_flag;
   const int* band_map;       // block-cyclic band (device), replaces band_lo/hi/shift
+  int diag_k;                // block-diagonal k ranges (eigensolver updates), complex only
   int a3d;                   // NoTrans: tA is the 3D single-box view (a_d0 multiple of a piece)
   const double* col_shift;   // residual epilogue (Alg.2 l.25): out -= col_shift[n] y2(m, n)
   const void* y2;
@@ -313,6 +328,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
     a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
     a.band_map = r.band_map;
+    a.diag_k = r.diag_k;
     a.a3d = r.a3d;
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
@@ -326,6 +342,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.use_beta = r.use_beta; a.band_lo = r.band_lo; a.band_hi = r.band_hi;
   a.band_shift = r.band_shift; a.upper_only = r.upper_only; a.abort_flag = r.abort_flag;
   a.band_map = r.band_map;
+  a.diag_k = r.diag_k;
   a.a3d = r.a3d;
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
@@ -685,6 +702,7 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->Wws = base + L.w;
   h->Rinv = base + L.rinv;
   h->B2ws = base + L.b2;
+  h->eigws = base + L.eig;
   h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
   h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
   if (h->nb > 0) {
@@ -1195,31 +1213,23 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   return st;
 }
 
-// Alg.2 l.23-28 (P:194-199, P:214): residual norms ||H v_j - lambda_j v_j|| of Ritz pairs.
-chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t lda, const void* V,
-                               int64_t ldv, int64_t ncols, const double* ritz, double* resid) {
-  if (!h || !A_local || !V || !ritz || !resid) return CHASE_EINVAL;
-  if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
-  for (int64_t j = 0; j < ncols; ++j)
-    if (!std::isfinite(ritz[j])) return CHASE_EINVAL;
-  if (!h->ws) return CHASE_ESTATE;
+// Alg.2 l.16 / l.23 "B2 <- Bcast(C2, ccomm)": the rows [c0, c0+n_c) (block-cyclic: the column
+// index set) of the C-layout block V, fetched from the rank(s) of the column communicator that
+// own them (one Bcast per owning block; a square grid needs one).  *y2 / *ldy2 point
+// to the B-layout copy (V itself on a 1x1 grid).
+static chase_status_t redistribute_b2(chase_handle_s* h, const void* V, int64_t ldv, int n,
+                                      const void** y2, int64_t* ldy2) {
   const size_t es = esize_of(h->dt), per = es / 8;
-  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
-    return CHASE_EINVAL;
-  if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;
-  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
-  const int n = (int)ncols;
-  CUDA_TRY(cudaMemcpyAsync(h->d_ritz, ritz, ncols * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-
+  const int64_t n_c = h->n_c, ldb = pad_ld(n_c);
   // l.23 B2 <- Bcast(C2, ccomm): rows [c0, c0+n_c) of V, from the rank(s) of this column
   // communicator that own them (one Bcast per owning block; a square grid needs one)
   const char* Vc = static_cast<const char*>(V);
   char* B2 = static_cast<char*>(h->B2ws);
-  const void* y2 = B2;
-  int64_t ldy2 = ldb;
+  *y2 = B2;
+  *ldy2 = ldb;
   if (h->p == 1 && h->q == 1) {
-    y2 = V;                                           // C- and B-layout coincide on a 1x1 grid
-    ldy2 = ldv;
+    *y2 = V;                                          // C- and B-layout coincide on a 1x1 grid
+    *ldy2 = ldv;
   } else if (h->nb > 0) {
     // block-cyclic: the owner gathers its rows of my column set, Bcast, scatter into B2
     ProfScope ps(h, CAT_ALLREDUCE, 0);
@@ -1270,6 +1280,29 @@ chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t ld
                                  rows * es, n, cudaMemcpyDeviceToDevice, h->stream));
     }
   }
+  return CHASE_OK;
+}
+
+// Alg.2 l.23-28 (P:194-199, P:214): residual norms ||H v_j - lambda_j v_j|| of Ritz pairs.
+chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t lda, const void* V,
+                               int64_t ldv, int64_t ncols, const double* ritz, double* resid) {
+  if (!h || !A_local || !V || !ritz || !resid) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
+  for (int64_t j = 0; j < ncols; ++j)
+    if (!std::isfinite(ritz[j])) return CHASE_EINVAL;
+  if (!h->ws) return CHASE_ESTATE;
+  const size_t es = esize_of(h->dt), per = es / 8;
+  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
+    return CHASE_EINVAL;
+  if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;
+  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
+  const int n = (int)ncols;
+  CUDA_TRY(cudaMemcpyAsync(h->d_ritz, ritz, ncols * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+
+  // l.23 B2 <- Bcast(C2, ccomm)
+  const void* y2 = nullptr;
+  int64_t ldy2 = 0;
+  STATUS_TRY(redistribute_b2(h, V, ldv, n, &y2, &ldy2));
   // l.24-25 B <- H C - ritzv B2: the odd-step HEMM with the shift term fused in the epilogue of
   // the first rank of the column communicator (linear, so it commutes with the AllReduce)
   CUtensorMap tA_t, tC;
@@ -1306,6 +1339,209 @@ chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t ld
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(resid, h->d_nrm, ncols * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return CHASE_OK;
+}
+
+// Alg.2 l.16-22: Rayleigh-Ritz on the orthonormal C-layout block V.
+chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_t lda, void* V,
+                                   int64_t ldv, int64_t ncols, double* ritz, int32_t* sweeps_out) {
+  if (!h || !A_local || !V || !ritz) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
+  if (!h->ws) return CHASE_ESTATE;
+  const size_t es = esize_of(h->dt);
+  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
+    return CHASE_EINVAL;
+  if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(jacobi_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, JAC_SMEM));
+    attr = true;
+  }
+  const int n = (int)ncols;
+  const int64_t n_r = h->n_r, n_c = h->n_c, ldb = pad_ld(n_c);
+  const bool cplx = h->dt == CHASE_C128;
+
+  // l.16 B2 <- Bcast(C2, ccomm)
+  const void* y2 = nullptr;
+  int64_t ldy2 = 0;
+  STATUS_TRY(redistribute_b2(h, V, ldv, n, &y2, &ldy2));
+  // l.17 B <- H C (the odd-step HEMM, no shift), AllReduce over ccomm
+  CUtensorMap tA_t, tC, tB2, tB;
+  STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &tC, V, n_r, n, ldv, ROLE_X));
+  char* Bc = static_cast<char*>(h->Bws);
+  {
+    GemmReq g{};
+    g.conj = true; g.tA = &tA_t; g.tX = &tC;
+    g.M = (int)n_c; g.N = n; g.K = (int)n_r;
+    g.out = Bc; g.ldo = ldb; g.alpha = 1.0;
+    ProfScope ps(h, CAT_HEMM_ODD, 1);
+    STATUS_TRY(run_gemm(h, g));
+  }
+  if (h->p > 1) STATUS_TRY(allreduce(h, Bc, (size_t)ldb * n, h->ccomm));
+  // l.18-19 A <- B2^H B, AllReduce over rcomm
+  const int64_t np = eig_np(n), L = np / 32;
+  char* E = h->eigws;
+  const size_t mat = align256((size_t)np * np * 16);
+  double2* Abuf[2] = {reinterpret_cast<double2*>(E), reinterpret_cast<double2*>(E + mat)};
+  double2* Ybuf[2] = {reinterpret_cast<double2*>(E + 2 * mat), reinterpret_cast<double2*>(E + 3 * mat)};
+  double2* Ubd = reinterpret_cast<double2*>(E + 4 * mat);
+  char* tail = E + 5 * mat;
+  double* d_w = reinterpret_cast<double*>(tail);
+  tail += align256(np * sizeof(double));
+  int* d_order = reinterpret_cast<int*>(tail);
+  tail += align256(np * sizeof(int));
+  int* d_perm = reinterpret_cast<int*>(tail);
+  tail += align256((size_t)(L + 1) * L * sizeof(int));
+  double* d_part = reinterpret_cast<double*>(tail);
+  double* d_off = d_part + 2 * JAC_RED_BLOCKS;
+  STATUS_TRY(make_role_map(h, &tB2, y2, n_c, n, ldy2, ROLE_A_TRANS));
+  STATUS_TRY(make_role_map(h, &tB, Bc, n_c, n, ldb, ROLE_X));
+  const int64_t ldq = pad_ld(n);                       // real quotient / sorted Y in the G region
+  {
+    GemmReq g{};
+    g.conj = true; g.tA = &tB2; g.tX = &tB;
+    g.M = n; g.N = n; g.K = (int)n_c;
+    g.out = cplx ? static_cast<void*>(Abuf[0]) : h->Gws;
+    g.ldo = cplx ? np : ldq; g.alpha = 1.0;
+    ProfScope ps(h, CAT_GRAM, 1);
+    STATUS_TRY(run_gemm(h, g));
+  }
+  if (h->q > 1)
+    STATUS_TRY(allreduce(h, cplx ? static_cast<void*>(Abuf[0]) : h->Gws, (size_t)(cplx ? np : ldq) * n, h->rcomm));
+  const unsigned TB = 256;
+  const unsigned g2 = (unsigned)((np * np + TB - 1) / TB);
+  if (!cplx)
+    real_to_complex_kernel<<<(unsigned)(((int64_t)n * n + TB - 1) / TB), TB, 0, h->stream>>>(
+        static_cast<const double*>(h->Gws), ldq, Abuf[0], np, n);
+  jacobi_init_kernel<<<g2, TB, 0, h->stream>>>(Abuf[0], Ybuf[0], Ubd, np, n, (int)np, 0.0);
+  CUDA_TRY(cudaGetLastError());
+
+  // l.20 HEEVD: parallel block Jacobi (eig.cuh).  Circle-method layouts over L blocks of 32:
+  // round r pairs (L-1, r) and ((r+i) mod (L-1), (r-i) mod (L-1)); pair i sits at positions
+  // (2i, 2i+1).  lay[r][pos] = logical block; perm tables map round r -> r+1 (and identity -> 0).
+  const int R = (int)(L - 1);
+  std::vector<std::vector<int>> lay(R, std::vector<int>(L));
+  for (int r = 0; r < R; ++r)
+    for (int i = 0; i < L / 2; ++i) {
+      int a, b;
+      if (i == 0) {
+        a = (int)L - 1;
+        b = r;
+      } else {
+        a = (r + i) % R;
+        b = (r - i + R) % R;
+      }
+      lay[r][2 * i] = a;
+      lay[r][2 * i + 1] = b;
+    }
+  // table t (t = 0..R-1): layout (t == 0 ? identity : lay[t-1]) -> lay[t]; table R: lay[R-1] -> lay[0]
+  std::vector<int> perm((size_t)(R + 1) * L);
+  for (int t = 0; t <= R; ++t) {
+    std::vector<int> inv(L);
+    const std::vector<int>* from = nullptr;
+    std::vector<int> ident(L);
+    for (int k = 0; k < L; ++k) ident[k] = k;
+    from = (t == 0) ? &ident : &lay[t - 1];
+    for (int k = 0; k < L; ++k) inv[(*from)[k]] = k;
+    const std::vector<int>& to = lay[t == R ? 0 : t];
+    for (int pos = 0; pos < L; ++pos) perm[(size_t)t * L + pos] = inv[to[pos]];
+  }
+  CUDA_TRY(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CUtensorMap mAnt[2], mAx[2], mYnt[2], mUx, mUt;
+  int a3dA[2], a3dY[2];
+  for (int b = 0; b < 2; ++b) {
+    STATUS_TRY(make_map(&mAx[b], Abuf[b], np, np, np, 16, 8, ZG_BN));
+    a3dA[b] = 0;
+    {
+      chase_handle_s tmp = *h;   // dtype-independent complex maps
+      tmp.dt = CHASE_C128;
+      STATUS_TRY(make_role_map(&tmp, &mAnt[b], Abuf[b], np, np, np, ROLE_A_NOTRANS, &a3dA[b]));
+      STATUS_TRY(make_role_map(&tmp, &mYnt[b], Ybuf[b], np, np, np, ROLE_A_NOTRANS, &a3dY[b]));
+    }
+  }
+  STATUS_TRY(make_map(&mUx, Ubd, np, np, np, 16, 8, ZG_BN));
+  STATUS_TRY(make_map(&mUt, Ubd, np, np, np, 16, 8, ZG_BM));
+  int cur = 0;
+  const dim3 gp((unsigned)g2);
+  auto permute = [&](int t) -> chase_status_t {
+    jacobi_perm_kernel<<<gp, TB, 0, h->stream>>>(Abuf[cur], Abuf[cur ^ 1], Ybuf[cur], Ybuf[cur ^ 1], np,
+                                                 (int)np, d_perm + (size_t)t * L);
+    CUDA_TRY(cudaGetLastError());
+    cur ^= 1;
+    return CHASE_OK;
+  };
+  auto zgemm_inplace = [&](bool conj, const CUtensorMap& tA, const CUtensorMap& tX, int a3d,
+                           double2* out, int K, int diag) -> chase_status_t {
+    ZGemmArgs a{};
+    a.M = (int)np; a.N = (int)np; a.K = K;
+    a.out = out; a.ldo = np; a.alpha = 1.0; a.a3d = a3d; a.diag_k = diag;
+    return launch_zgemm(h, conj, tA, tX, a);
+  };
+  ProfScope ps_eig(h, CAT_OTHER, 0);
+  if (L > 2) STATUS_TRY(permute(0));
+  int sweeps = 0;
+  const int max_sweeps = 40;
+  std::vector<double> off(2);
+  for (; sweeps < max_sweeps; ++sweeps) {
+    for (int r = 0; r < (L > 2 ? R : 1); ++r) {
+      jacobi_pair_kernel<<<(unsigned)(np / JAC_PW), JAC_THREADS, JAC_SMEM, h->stream>>>(Abuf[cur], np, Ubd, np, 15);
+      CUDA_TRY(cudaGetLastError());
+      STATUS_TRY(zgemm_inplace(false, mAnt[cur], mUx, a3dA[cur], Abuf[cur], JAC_PW, 1));   // A U
+      STATUS_TRY(zgemm_inplace(true, mUt, mAx[cur], 0, Abuf[cur], 2 * JAC_PW, 2));          // U^H A
+      STATUS_TRY(zgemm_inplace(false, mYnt[cur], mUx, a3dY[cur], Ybuf[cur], JAC_PW, 1));   // Y U
+      h->launches[CAT_OTHER] += 4;
+      if (L > 2) STATUS_TRY(permute(r + 1));
+    }
+    jacobi_offnorm_kernel<<<JAC_RED_BLOCKS, 256, 0, h->stream>>>(Abuf[cur], np, (int)np, d_part);
+    jacobi_offnorm_final<<<1, 32, 0, h->stream>>>(d_part, JAC_RED_BLOCKS, d_off);
+    CUDA_TRY(cudaMemcpyAsync(off.data(), d_off, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (!(off[0] > 1e-28 * off[1])) {
+      ++sweeps;
+      break;
+    }
+  }
+  // eigenvalues in physical order; physical column -> logical index; drop the padding; sort
+  std::vector<double> w(np);
+  jacobi_diag_kernel<<<(unsigned)((np + 255) / 256), 256, 0, h->stream>>>(Abuf[cur], np, (int)np, d_w);
+  CUDA_TRY(cudaMemcpyAsync(w.data(), d_w, np * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  const std::vector<int>& fin = (L > 2) ? lay[0] : std::vector<int>{0, 1};
+  std::vector<int> cols;
+  for (int pos = 0; pos < np; ++pos) {
+    const int logical = fin[pos / 32] * 32 + pos % 32;
+    if (logical < n) cols.push_back(pos);
+  }
+  std::stable_sort(cols.begin(), cols.end(), [&](int a, int b) { return w[a] < w[b]; });
+  for (int k = 0; k < n; ++k) ritz[k] = w[cols[k]];
+  CUDA_TRY(cudaMemcpyAsync(d_order, cols.data(), n * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  const unsigned gn = (unsigned)(((int64_t)n * n + 255) / 256);
+  if (cplx)
+    jacobi_gather_kernel<double2><<<gn, 256, 0, h->stream>>>(Ybuf[cur], np, n, d_order,
+                                                              static_cast<double2*>(h->Gws), ldq);
+  else
+    jacobi_gather_kernel<double><<<gn, 256, 0, h->stream>>>(Ybuf[cur], np, n, d_order,
+                                                             static_cast<double*>(h->Gws), ldq);
+  CUDA_TRY(cudaGetLastError());
+  // l.21 C <- C2 A (the eigenvectors), into W then back into V (l.22 C2 <- C is the caller's)
+  CUtensorMap tV, tY;
+  int a3dV = 0;
+  STATUS_TRY(make_role_map(h, &tV, V, n_r, n, ldv, ROLE_A_NOTRANS, &a3dV));
+  STATUS_TRY(make_role_map(h, &tY, h->Gws, n, n, ldq, ROLE_X));
+  char* W = static_cast<char*>(h->Wws);
+  const int64_t ldw = pad_ld(n_r);
+  {
+    GemmReq g{};
+    g.conj = false; g.tA = &tV; g.tX = &tY; g.a3d = a3dV;
+    g.M = (int)n_r; g.N = n; g.K = n;
+    g.out = W; g.ldo = ldw; g.alpha = 1.0;
+    ProfScope ps(h, CAT_TRSM, 1);
+    STATUS_TRY(run_gemm(h, g));
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(V, ldv * es, W, ldw * es, n_r * es, n, cudaMemcpyDeviceToDevice, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (sweeps_out) *sweeps_out = sweeps;
   return CHASE_OK;
 }
 

@@ -52,6 +52,7 @@ struct DGemmArgs {
   int upper_only;
   const int* abort_flag;
   const int* band_map;     // non-null (block-cyclic): see zgemm.cuh
+  int diag_k;              // block-diagonal k ranges: see zgemm.cuh
   int a3d;                 // NoTrans only: tmA is the 3D view {16 doubles, k, m/16} -> 1 TMA/stage
   const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (Alg.2 l.25)
   const double* y2;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   if (g.upper_only && m0 > n0 + DG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT = (g.K + DG_BK - 1) / DG_BK;
+  const int dk = g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0);   // per-CTA k offset
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < DG_STAGES; ++s) {
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     mbar_arrive_expect_tx(&full[s], DG_STAGE_BYTES);
     uint8_t* sa = smem + s * DG_STAGE_BYTES;
     uint8_t* sx = sa + DG_A_BYTES;
-    const int k0 = kt * DG_BK;
+    const int k0 = kt * DG_BK + dk;
     if (TRANS) {
       tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);     // box 16 k x 128 m
     } else {

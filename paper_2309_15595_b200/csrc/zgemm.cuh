@@ -67,6 +67,8 @@ struct ZGemmArgs {
   int band_shift;
   int upper_only;          // skip CTAs whose tile lies strictly below the diagonal (m > n)
   const int* abort_flag;   // non-null: skip the whole GEMM when *abort_flag != 0 (POTRF info)
+  int diag_k;              // block-diagonal right/left factor (Jacobi eigensolver updates):
+                           //   1: the k range of n-tile n0 starts at n0; 2: of m-tile m0 at m0
   const int* band_map;     // non-null (block-cyclic): out row m subtracts c * xin[band_map[m], n]
                            //   when band_map[m] >= 0; replaces [band_lo, band_hi)
   int a3d;                 // NoTrans only: tmA is the 3D view {8 complex, k, m/8} -> 1 TMA/stage
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
+  const int dk = g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0);   // per-CTA k offset
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ZG_STAGES; ++s) {
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     uint8_t* sx = sa + ZG_A_BYTES;
 #pragma unroll
     for (int u = 0; u < ZG_KS; ++u) {
-      const int k0 = kt * ZG_BK + 8 * u;
+      const int k0 = kt * ZG_BK + 8 * u + dk;
       uint8_t* sau = sa + u * ZG_A_SLAB;
       if (CONJ) {
         // opA[m][k] = conj(A[k][m]); A rows (k) contiguous: one 128 x 8 box, row = m

@@ -73,25 +73,34 @@ def main():
     dist.broadcast_object_list(obj, src=0)
     ritz = obj[0]
     resid = h.residuals(Ad, Vd, ritz)
+    # Rayleigh-Ritz (Alg.2 l.16-22) on the orthonormal Q
+    theta, _ = h.rayleigh_ritz(Ad, Vd)
+    torch.cuda.synchronize()
+    Xr = Vd.T.cpu().numpy().T.copy()
     g = [None] * world
-    dist.all_gather_object(g, (rank, myrow, mycol, rows, n_r, n_c, Vf, Q, rec, mv, qr, resid, ritz, repeat_equal))
+    dist.all_gather_object(g, (rank, myrow, mycol, rows, n_r, n_c, Vf, Q, rec, mv, qr, resid, ritz, repeat_equal,
+                               theta, Xr))
     if rank == 0:
         Vfull = np.zeros((N, n), dtype=dt)
         Qfull = np.zeros((N, n), dtype=dt)
+        Xfull = np.zeros((N, n), dtype=dt)
         replica = 0.0
         for x in g:
             if x[2] == 0:
                 Vfull[x[3]] = x[6]
                 Qfull[x[3]] = x[7]
+                Xfull[x[3]] = x[15]
         for x in g:
             replica = max(replica, float(np.max(np.abs(x[6] - Vfull[x[3]]))),
-                          float(np.max(np.abs(x[7] - Qfull[x[3]]))))
+                          float(np.max(np.abs(x[7] - Qfull[x[3]]))),
+                          float(np.max(np.abs(x[15] - Xfull[x[3]]))))
         np.savez(out, V=Vfull, Q=Qfull, replica=replica, est=est,
                  variants=np.array([x[10]["variant"] for x in g]), passes=np.array([x[10]["passes"] for x in g]),
                  status=np.array([x[10]["status"] for x in g]), mv=np.array([x[9] for x in g]),
                  recs=np.array([str(x[8]) for x in g]), ranks=np.array([[x[1], x[2], x[4], x[5]] for x in g]),
                  resid=np.array([x[11] for x in g]), ritz=g[0][12],
-                 repeat_equal=np.array([x[13] for x in g]))
+                 repeat_equal=np.array([x[13] for x in g]), X=Xfull,
+                 theta=np.array([x[14] for x in g]))
     h.close()
     dist.destroy_process_group()
 

@@ -97,6 +97,12 @@ def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode, nb):
     rres = oracle.residuals(A, Q, res["ritz"])
     assert np.all(res["resid"] == res["resid"][0])
     assert np.max(np.abs(res["resid"][0] - rres) / rres) <= 1e-10
+    # Rayleigh-Ritz (Alg.2 l.16-22): Ritz values identical on every rank and equal to the oracle's
+    theta_ref, X_ref = oracle.rayleigh_ritz(A, Q)
+    assert np.all(res["theta"] == res["theta"][0])
+    assert np.max(np.abs(res["theta"][0] - theta_ref)) <= 1e-12 * np.max(np.abs(theta_ref))
+    X = res["X"]
+    assert np.linalg.norm(X.conj().T @ X - np.eye(n)) <= 1e-11
 
 
 FULL = [("C3", (2, 1)), ("C3", (2, 2)), ("C3", (2, 4)), ("C4", (2, 2)), ("C4", (2, 4)),
