@@ -1482,10 +1482,13 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
   if (L > 2) STATUS_TRY(permute(0));
   int sweeps = 0;
   const int max_sweeps = 40;
+  // one inner sweep per pair visit: the outer block-Jacobi sweeps finish the job (measured
+  // fastest: n = 3000 in 13 sweeps, 2.0 s vs 2.8 s with inner convergence)
+  static const int inner_sweeps = getenv("CHASE_JAC_INNER") ? atoi(getenv("CHASE_JAC_INNER")) : 1;
   std::vector<double> off(2);
   for (; sweeps < max_sweeps; ++sweeps) {
     for (int r = 0; r < (L > 2 ? R : 1); ++r) {
-      jacobi_pair_kernel<<<(unsigned)(np / JAC_PW), JAC_THREADS, JAC_SMEM, h->stream>>>(Abuf[cur], np, Ubd, np, 15);
+      jacobi_pair_kernel<<<(unsigned)(np / JAC_PW), JAC_THREADS, JAC_SMEM, h->stream>>>(Abuf[cur], np, Ubd, np, inner_sweeps);
       CUDA_TRY(cudaGetLastError());
       STATUS_TRY(zgemm_inplace(false, mAnt[cur], mUx, a3dA[cur], Abuf[cur], JAC_PW, 1));   // A U
       STATUS_TRY(zgemm_inplace(true, mUt, mAx[cur], 0, Abuf[cur], 2 * JAC_PW, 2));          // U^H A

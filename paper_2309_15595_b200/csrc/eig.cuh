@@ -116,17 +116,35 @@ __global__ void __launch_bounds__(JAC_THREADS)
       }
       __syncthreads();
     }
-    // stop when this sweep rotated nothing or the block is diagonal to roundoff
-    if (tid == 0) {
+    // stop when this sweep rotated nothing or the block is diagonal to roundoff (parallel,
+    // fixed-order reduction)
+    {
       double off = 0.0, tot = 0.0;
-      for (int c = 0; c < JAC_PW; ++c)
-        for (int r = 0; r < JAC_PW; ++r) {
-          const double v = S[r][c].x * S[r][c].x + S[r][c].y * S[r][c].y;
-          tot += v;
-          if (r != c) off += v;
+      for (int idx = tid; idx < JAC_PW * JAC_PW; idx += JAC_THREADS) {
+        const int r = idx % JAC_PW, c = idx / JAC_PW;
+        const double v = S[r][c].x * S[r][c].x + S[r][c].y * S[r][c].y;
+        tot += v;
+        if (r != c) off += v;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        off += __shfl_xor_sync(0xffffffffu, off, o);
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      }
+      __shared__ double w_off[JAC_THREADS / 32], w_tot[JAC_THREADS / 32];
+      if ((tid & 31) == 0) {
+        w_off[tid >> 5] = off;
+        w_tot[tid >> 5] = tot;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double o2 = 0.0, t2 = 0.0;
+        for (int w = 0; w < JAC_THREADS / 32; ++w) {
+          o2 += w_off[w];
+          t2 += w_tot[w];
         }
-      s_off = off;
-      s_tot = tot;
+        s_off = o2;
+        s_tot = t2;
+      }
     }
     __syncthreads();
     if (!s_rot || s_off <= 1e-32 * s_tot) break;
