@@ -38,7 +38,8 @@ typedef enum {
   CHASE_ECUDA = 5,    /* CUDA runtime / driver failure                                        */
   CHASE_ENCCL = 6,    /* NCCL failure                                                         */
   CHASE_ENOMEM = 7,   /* workspace missing or too small                                       */
-  CHASE_ESTATE = 8    /* call sequence error (e.g. no workspace set)                          */
+  CHASE_ESTATE = 8,   /* call sequence error (e.g. no workspace set)                          */
+  CHASE_ENOCONV = 9   /* chase_solve: not converged within max_iter (partial results)          */
 } chase_status_t;
 
 typedef enum { CHASE_R64 = 1, CHASE_C128 = 2 } chase_dtype_t;
@@ -235,6 +236,34 @@ chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int myc
  * CHASE_ECUDA, CHASE_ENCCL. */
 chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols, double cond_est,
                             chase_stats_t* stats, int32_t* info);
+
+/* ---------------------------------------------------------------------------------------
+ * The full ChASE iteration -- Alg.2 for the nev lowest eigenpairs:
+ * Lanczos bounds (Alg.1 l.2: 4 runs x 25 steps, b_sup = max theta + beta_k, mu_1 = min theta,
+ * mu_ne from the Ritz-value density), then repeat {bounds update (l.6-7), degreeOpt (l.9, when
+ * opt), Filter (l.12), CondEst (l.13), 1D-CAQR (l.14), C/C2 copies (l.15), Rayleigh-Ritz
+ * (l.16-22), residuals (l.23-28), locking (l.29-30)} until nev pairs are locked.  Block
+ * distribution only.  Collective; identical arguments on every rank.
+ *  V        device, in/out, C-layout n_r x (nev+nex): initial vectors (init_random == 0: the
+ *           caller's approximate eigenvectors) or filled with counter-based seeded
+ *           Gaussians keyed by global row (init_random != 0); on return the first nev columns
+ *           are the eigenvectors (ascending).
+ *  tol      residual tolerance on ||H v - lambda v|| / max(|mu_1|, |b_sup|) (1e-10).
+ *  deg      initial degree (even: 20), deg_max cap (even: 36); opt: degreeOpt on.
+ *  lambda, resid  host out, nev+nex values (first nev: the locked eigenpairs).
+ * Returns CHASE_OK when nev pairs converged, CHASE_ENOCONV after max_iter (partial results),
+ * or the error of a failing step. */
+typedef struct {
+  int64_t matvecs;      /* filter + Rayleigh-Ritz + residual + Lanczos single-vector products */
+  int32_t iterations;
+  int32_t locked;
+  int32_t reserved;
+  double b_sup, mu_1, mu_ne;   /* Lanczos bounds of the first iteration / last update */
+} chase_solve_stats_t;
+chase_status_t chase_solve(chase_handle_t h, const void* A_local, int64_t lda, void* V, int64_t ldv,
+                           int64_t nev, int64_t nex, double tol, int32_t deg, int32_t deg_max,
+                           int32_t max_iter, int32_t opt, uint64_t seed, int32_t init_random,
+                           double* lambda, double* resid, chase_solve_stats_t* stats);
 
 /* ---------------------------------------------------------------------------------------
  * Rayleigh-Ritz -- Alg.2 l.16-22 on the orthonormal

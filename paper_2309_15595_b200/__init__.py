@@ -24,7 +24,7 @@ CHASE_R64, CHASE_C128 = 1, 2
 CHASE_QR_CHOL1, CHASE_QR_CHOL2, CHASE_QR_SHIFTED = 1, 2, 3
 STATUS = {0: "CHASE_OK", 1: "CHASE_EINVAL", 2: "CHASE_EDEGREE", 3: "CHASE_EBOUNDS",
           4: "CHASE_ECHOL", 5: "CHASE_ECUDA", 6: "CHASE_ENCCL", 7: "CHASE_ENOMEM",
-          8: "CHASE_ESTATE"}
+          8: "CHASE_ESTATE", 9: "CHASE_ENOCONV"}
 PROFILE_CATEGORIES = ("hemm_odd", "hemm_even", "allreduce", "gram", "potrf", "trsm", "other", "reserved")
 
 # every symbol include/chase.h declares (checked by tests/test_abi.py)
@@ -35,7 +35,7 @@ EXPORTED = (
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
     "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
     "chase_set_fused_workspace", "chase_create_cyclic", "chase_local_indices",
-    "chase_cyclic_indices", "chase_rayleigh_ritz",
+    "chase_cyclic_indices", "chase_rayleigh_ritz", "chase_solve",
 )
 
 
@@ -53,6 +53,12 @@ class chase_stats_t(ctypes.Structure):
     _fields_ = [("matvecs", ctypes.c_int64), ("steps", ctypes.c_int32),
                 ("qr_variant", ctypes.c_int32), ("qr_passes", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
+
+
+class chase_solve_stats_t(ctypes.Structure):
+    _fields_ = [("matvecs", ctypes.c_int64), ("iterations", ctypes.c_int32), ("locked", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("b_sup", ctypes.c_double), ("mu_1", ctypes.c_double),
+                ("mu_ne", ctypes.c_double)]
 
 
 class chase_step_record_t(ctypes.Structure):
@@ -95,6 +101,8 @@ def load() -> ctypes.CDLL:
         "chase_residuals": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "chase_fused_workspace_size": (I32, [V, ctypes.POINTER(ctypes.c_size_t)]),
         "chase_rayleigh_ritz": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(I32)]),
+        "chase_solve": (I32, [V, V, I64, V, I64, I64, I64, D, I32, I32, I32, I32, ctypes.c_uint64, I32,
+                              ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(chase_solve_stats_t)]),
         "chase_set_fused_workspace": (I32, [V, V, ctypes.POINTER(ctypes.c_uint64), I32]),
         "chase_shift_value": (D, [I64, I64, D]),
         "chase_profile_enable": (I32, [V, I32]),
@@ -308,6 +316,28 @@ def chase_rayleigh_ritz(h, A_local, V, ncols: int | None = None):
     return out, sw.value
 
 
+def chase_solve(h, A_local, V, nev: int, nex: int, tol: float = 1e-10, deg: int = 20,
+                deg_max: int = 36, max_iter: int = 25, opt: bool = True, seed: int = 0,
+                init_random: bool = True, raise_on_error: bool = True):
+    """Full ChASE iteration (Alg.2).  V: C-layout n_r x (nev+nex) device block (in: initial
+    vectors unless init_random; out: eigenvectors).  Returns dict(status, lambda, resid, stats)."""
+    a_ptr, lda = _colmajor(A_local, "A_local")
+    v_ptr, ldv = _colmajor(V, "V")
+    ne = nev + nex
+    lam = np.empty(ne, dtype=np.float64)
+    res = np.empty(ne, dtype=np.float64)
+    st = chase_solve_stats_t()
+    s = load().chase_solve(h, a_ptr, lda, v_ptr, ldv, nev, nex, float(tol), deg, deg_max, max_iter,
+                           1 if opt else 0, seed, 1 if init_random else 0,
+                           lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                           res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(st))
+    if raise_on_error and s not in (0, 9):
+        _check(s, "chase_solve")
+    return {"status": s, "lambda": lam, "resid": res,
+            "stats": {"matvecs": st.matvecs, "iterations": st.iterations, "locked": st.locked,
+                      "b_sup": st.b_sup, "mu_1": st.mu_1, "mu_ne": st.mu_ne}}
+
+
 def chase_cond_est(ritz, c: float, e: float, degrees, locked: int = 0) -> float:
     """Alg.5 over the n = len(degrees) vectors; ritz needs at least n values (ascending)."""
     r = np.ascontiguousarray(np.asarray(ritz, dtype=np.float64))
@@ -369,6 +399,9 @@ class Chase:
 
     def cholqr(self, V, cond_est, ncols=None, raise_on_error=True):
         return chase_cholqr(self.h, V, cond_est, ncols, raise_on_error)
+
+    def solve(self, A_local, V, nev, nex, **kw):
+        return chase_solve(self.h, A_local, V, nev, nex, **kw)
 
     def rayleigh_ritz(self, A_local, V, ncols=None):
         return chase_rayleigh_ritz(self.h, A_local, V, ncols)

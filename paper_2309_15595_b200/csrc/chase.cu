@@ -129,6 +129,8 @@ struct chase_handle_s {
   void* Rinv = nullptr;     // 64 x n_max (inverted diagonal blocks of R)
   void* B2ws = nullptr;     // n_c x n_max (C redistributed into B-layout, Alg.2 l.23)
   char* eigws = nullptr;    // Jacobi eigensolver region (see eig_bytes)
+  char* c2ws = nullptr;     // solver: C2
+  char* lanws = nullptr;    // solver: Lanczos basis
   double* d_ritz = nullptr;
   double* d_nrm = nullptr;
   int* d_info = nullptr;
@@ -196,8 +198,10 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, info, s, total;
 };
+constexpr int LANCZOS_K = 25;       // Lanczos steps per run (bounds, Alg.1 l.2)
+constexpr int LANCZOS_RUNS = 4;     // independent runs pooled for the DoS estimate
 // Jacobi eigensolver buffers (Rayleigh-Ritz): A ping-pong, Y ping-pong, U_bd (np x np complex
 // each, np = n_max rounded up to 64) + eigenvalues, order, permutation tables, partial sums.
 static int64_t eig_np(int64_t n) { return (n + JAC_PW - 1) / JAC_PW * JAC_PW; }
@@ -231,6 +235,10 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)(h->n_r + 3 * h->n_c) * sizeof(int));
   L.eig = off;                                          // Rayleigh-Ritz eigensolver
   off += eig_bytes(h->n_max);
+  L.c2 = off;                                           // solver: C2 (Alg.2 buffers C2 / B2)
+  off += align256((size_t)pad_ld(h->n_r) * h->n_max * es);
+  L.lan = off;                                          // solver: Lanczos basis + scalars
+  off += align256((size_t)pad_ld(h->n_r) * (LANCZOS_K + 2) * es) + 4096;
   L.info = off;
   off += 256;
   L.s = off;
@@ -563,6 +571,7 @@ const char* chase_status_string(chase_status_t s) {
     case CHASE_ENCCL: return "CHASE_ENCCL: NCCL failure";
     case CHASE_ENOMEM: return "CHASE_ENOMEM: workspace missing or too small";
     case CHASE_ESTATE: return "CHASE_ESTATE: invalid call sequence";
+    case CHASE_ENOCONV: return "CHASE_ENOCONV: not converged within max_iter (partial results)";
   }
   return "CHASE_?: unknown status";
 }
@@ -703,6 +712,8 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->Rinv = base + L.rinv;
   h->B2ws = base + L.b2;
   h->eigws = base + L.eig;
+  h->c2ws = base + L.c2;
+  h->lanws = base + L.lan;
   h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
   h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
   if (h->nb > 0) {
@@ -1609,3 +1620,5 @@ chase_status_t chase_destroy(chase_handle_t h) {
 }
 
 }  // extern "C"
+
+#include "solver.inc"

@@ -127,3 +127,25 @@ def test_full_size_grid(tmp_path, name, grid):
         assert res["record_equal"], res
         assert res["qr_variant"] == res["oracle_variant"], res
         assert res["orth"] <= 1e-12, res
+
+
+@pytest.mark.parametrize("grid", [(1, 1), (2, 1), (1, 2), (2, 2)])
+def test_solve_grid(tmp_path, grid):
+    """the full ChASE loop on a p x q grid converges to the lowest nev
+    eigenpairs of Uniform[0,1] (N = 400); identical eigenvalues on every rank."""
+    p, q = grid
+    if ngpus() < p * q:
+        pytest.skip(f"needs {p * q} GPUs")
+    N, nev, nex = 400, 40, 20
+    out = str(tmp_path / "solve.npz")
+    r = torchrun(p * q, [os.path.join(ROOT, "tests", "mp_solve_worker.py"), str(p), str(q), str(N),
+                         str(nev), str(nex), out], 900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = np.load(out)
+    lam = ci.uniform_spectrum(N)
+    assert int(res["status"]) == 0 and bool(res["same"])
+    assert np.max(np.abs(res["lam"][:nev] - lam[:nev])) <= 1e-9
+    A = ci.dense_from_spectrum(lam, 21, True)
+    X = res["X"][:, :nev]
+    rr = oracle.residuals(A, X, res["lam"][:nev])
+    assert np.max(rr) <= 1e-9

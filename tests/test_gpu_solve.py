@@ -1,0 +1,58 @@
+"""The full ChASE iteration (chase_solve, Alg.2) on the GPU: converges to the lowest nev
+eigenpairs of matrices with a prescribed spectrum; eigenvalues against the exact spectrum and
+residuals/orthogonality recomputed independently on the host."""
+import numpy as np
+import pytest
+
+import chase_inputs as ci
+import oracle
+import paper_2309_15595_b200 as cb
+from gpu_util import dev, host
+
+pytestmark = pytest.mark.gpu
+
+
+def run(A, nev, nex, complex_, **kw):
+    import torch
+    N = A.shape[0]
+    h = cb.Chase(cb.CHASE_C128 if complex_ else cb.CHASE_R64, N, nev + nex)
+    Ad = dev(A)
+    Vd = dev(np.zeros((N, nev + nex), dtype=A.dtype))
+    out = h.solve(Ad, Vd, nev, nex, **kw)
+    torch.cuda.synchronize()
+    X = host(Vd)
+    h.close()
+    return out, X
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+def test_diag_1_to_200(complex_):
+    """diag(1..200) rotated by a Haar Q, nev = 20, nex = 10, tol 1e-10 ->
+    Lambda = 1..20 to 1e-9, all residuals <= tol."""
+    lam = np.arange(1, 201, dtype=np.float64)
+    A = ci.dense_from_spectrum(lam, 3, complex_)
+    out, X = run(A, 20, 10, complex_, tol=1e-10)
+    assert out["status"] == 0, out
+    L = out["lambda"][:20]
+    assert np.max(np.abs(L - lam[:20])) <= 1e-9
+    assert np.all(out["resid"][:20] <= 1e-10)
+    scale = max(abs(out["stats"]["mu_1"]), abs(out["stats"]["b_sup"]))
+    r = oracle.residuals(A, X[:, :20], L) / scale
+    assert np.all(r <= 2e-10)
+    assert np.linalg.norm(X[:, :20].conj().T @ X[:, :20] - np.eye(20)) <= 1e-11
+
+
+@pytest.mark.parametrize("opt", [True, False])
+def test_uniform_1000(opt):
+    """Uniform spectrum on [0, 1], N = 1000, nev = 100, nex = 40 (SPEC S:622 protocol)."""
+    N, nev, nex = 1000, 100, 40
+    lam = ci.uniform_spectrum(N)
+    A = ci.dense_from_spectrum(lam, 11, True)
+    out, X = run(A, nev, nex, True, tol=1e-10, opt=opt, max_iter=30)
+    assert out["status"] == 0, out
+    assert np.max(np.abs(out["lambda"][:nev] - lam[:nev])) <= 1e-9
+    scale = max(abs(out["stats"]["mu_1"]), abs(out["stats"]["b_sup"]))
+    r = oracle.residuals(A, X[:, :nev], out["lambda"][:nev]) / scale
+    assert np.all(r <= 2e-10)
+    assert out["stats"]["b_sup"] >= lam[-1] - 1e-6          # Lanczos upper bound
+    print(out["stats"])
