@@ -17,7 +17,8 @@ Every function here is pinned; none is "parity unpinned".
 """
 from .filter import chebyshev_scalars, chebyshev_filter, filter_schedule, filter_record  # noqa: F401
 from .qr import (gram, potrf_upper, trsm_right_upper, shift_value, cholesky_qr, caqr,  # noqa: F401
-                 cond_est, select_variant, householder_qr, frobenius_sq)
+                 cond_est, select_variant, householder_qr, householder_factor, larfg,
+                 frobenius_sq)
 from .grid import distributed_filter  # noqa: F401
 from .residual import residuals  # noqa: F401
 from .rayleigh_ritz import rayleigh_ritz  # noqa: F401

@@ -7,7 +7,9 @@
   shift_value       Alg.4 l.6  s = 11 (m n + n (n + 1)) u norm
   caqr              Alg.4      condition-driven dispatch
   cond_est          Alg.5      condition estimate of the filtered block
-  householder_qr    pin only (HHQR, the paper's ScaLAPACK fallback)
+  householder_qr    Alg.4 l.9 "X <- ScaLAPACK-HHQR(X, comm)": LAPACK-
+                    convention Householder QR (xGEQR2 + xUNG2R, reflectors of xLARFG), Q
+                    normalised so diag(R) is positive real (reading #33); also a CholeskyQR pin
 
 Readings (DESIGN.md): u = 2^-53 (#10); m = global row count, n = columns QR'd (#11);
 norm = squared Frobenius norm of X (#12); shifted path = 1 shifted pass + CholeskyQR2 (#13);
@@ -24,7 +26,7 @@ import numpy as np
 
 U_ROUNDOFF = 2.0 ** -53          # unit round-off of IEEE double (reading #10)
 
-CHOL1, CHOL2, SHIFTED = 1, 2, 3  # same numbering as include/chase.h chase_qr_variant_t
+CHOL1, CHOL2, SHIFTED, HOUSEHOLDER = 1, 2, 3, 4  # include/chase.h chase_qr_variant_t
 OK, ECHOL = 0, 4
 
 
@@ -93,39 +95,44 @@ def select_variant(est: float) -> int:
 
 
 def _shifted(X: np.ndarray, m_global: int):
-    """Alg.4 l.3-12: one shifted pass then CholeskyQR2.  Returns (Q, info, passes)."""
+    """Alg.4 l.3-12: one shifted pass then CholeskyQR2; a failing shifted POTRF reverts to
+    HHQR (l.8-9).  Returns (Q, info, passes, hhqr_used)."""
     n = X.shape[1]
     G = gram(X)
     norm = frobenius_sq(X)
     s = shift_value(m_global, n, norm)
     R, info = potrf_upper(G + s * np.eye(n, dtype=G.dtype))
     if info != 0:
-        return X, info, 0          # HHQR fallback is out of scope: report (reading #15)
+        return householder_qr(X), info, 0, True          # Alg.4 l.9 (P:299)
     X = trsm_right_upper(X, R)
-    Q, info, p = cholesky_qr(X, 2)
-    return Q, info, 1 + p
+    Q, info2, p = cholesky_qr(X, 2)
+    if info2 != 0:                  # reading #33: HHQR on the last successful pass output
+        return householder_qr(Q), info2, 1 + p, True
+    return Q, 0, 1 + p, False
 
 
 def caqr(X: np.ndarray, est: float):
     """Alg.4 (1D-CAQR for ChASE) on the global N x n block X.
 
-    Returns dict(Q, status, variant, passes, info) where variant is the branch actually
-    executed (escalation per reading #14)."""
+    Returns dict(Q, status, variant, passes, info): variant is the branch actually executed
+    (escalation per reading #14; HOUSEHOLDER when the HHQR fallback ran, reading #33), passes
+    the number of successful Cholesky passes, info the 1-based pivot of the last failed POTRF
+    (0 if none failed)."""
     if not (est >= 1.0):
         raise ValueError("cond_est must be >= 1 (S:397)")
     m = X.shape[0]
     v = select_variant(est)
-    if v == SHIFTED:
-        Q, info, passes = _shifted(X, m)
-        return dict(Q=Q, status=OK if info == 0 else ECHOL, variant=SHIFTED, passes=passes, info=info)
-    deg = 1 if v == CHOL1 else 2
-    Q, info, passes = cholesky_qr(X, deg)
-    if info == 0:
-        return dict(Q=Q, status=OK, variant=v, passes=passes, info=0)
-    if passes == 0:                # first POTRF failed, X untouched: escalate (reading #14)
-        Q, info, p2 = _shifted(X, m)
-        return dict(Q=Q, status=OK if info == 0 else ECHOL, variant=SHIFTED, passes=p2, info=info)
-    return dict(Q=Q, status=ECHOL, variant=v, passes=passes, info=info)
+    if v != SHIFTED:
+        deg = 1 if v == CHOL1 else 2
+        Q, info, passes = cholesky_qr(X, deg)
+        if info == 0:
+            return dict(Q=Q, status=OK, variant=v, passes=passes, info=0)
+        if passes > 0:              # reading #33: later failure -> HHQR on the current X
+            return dict(Q=householder_qr(Q), status=OK, variant=HOUSEHOLDER, passes=passes,
+                        info=info)
+        # first POTRF failed, X untouched: escalate (reading #14)
+    Q, info, passes, hh = _shifted(X, m)
+    return dict(Q=Q, status=OK, variant=HOUSEHOLDER if hh else SHIFTED, passes=passes, info=info)
 
 
 def cond_est(ritz, c: float, e: float, degs, locked: int) -> float:
@@ -149,33 +156,52 @@ def cond_est(ritz, c: float, e: float, degs, locked: int) -> float:
     return rho(t) ** d * rho(tp) ** (dM - d)
 
 
-def householder_qr(X: np.ndarray) -> np.ndarray:
-    """Thin Q of a Householder QR of X (m >= n), normalised so diag(R) is positive real.
-    Used only to pin CholeskyQR (same Q up to rounding for full-rank X)."""
+def larfg(alpha, x: np.ndarray):
+    """The elementary reflector of LAPACK xLARFG, which ScaLAPACK's HHQR applies:
+        H^H (alpha; x) = (beta; 0),  H = I - tau v v^H,  v = (1; x / (alpha - beta)),
+        beta = -sign(Re alpha) ||(alpha; x)||_2  (real),  tau = (beta - alpha) / beta;
+    H = I (tau = 0, beta = alpha) when x = 0 and alpha is real.  Returns (tau, beta, v[1:])."""
+    xnorm2 = float(np.vdot(x, x).real)
+    a = complex(alpha)
+    if xnorm2 == 0.0 and a.imag == 0.0:
+        return 0.0, a.real, x.copy()
+    beta = -math.copysign(math.sqrt(abs(a) ** 2 + xnorm2), a.real)
+    tau = (beta - alpha) / beta
+    return tau, beta, x / (alpha - beta)
+
+
+def householder_factor(X: np.ndarray):
+    """Unblocked Householder QR, LAPACK xGEQR2 then xUNG2R, column by column:
+        k = 0..n-1: (tau_k, beta_k, v_k) = larfg(A[k, k], A[k+1:, k]);
+                    A[k:, k+1:] <- H_k^H A[k:, k+1:]
+        Q = H_0 H_1 ... H_{n-1} [I_n; 0]   (applied right to left).
+    Returns (Q, beta): R = Q^H X is upper triangular with diagonal beta (real)."""
     A = np.array(X, dtype=np.result_type(X.dtype, np.float64), copy=True)
     m, n = A.shape
-    vs = []
+    taus, betas, vs = [], [], []
     for k in range(n):
-        x = A[k:, k].copy()
-        alpha = np.linalg.norm(x)
-        if alpha == 0.0:
-            vs.append(None)
-            continue
-        ph = x[0] / abs(x[0]) if x[0] != 0 else 1.0
-        v = x.copy()
-        v[0] += ph * alpha
-        v /= np.linalg.norm(v)
-        A[k:, k:] -= 2.0 * np.outer(v, v.conj() @ A[k:, k:])
-        vs.append(v)
-    # form Q = H_1 ... H_n [I_n; 0]
+        tau, beta, v = larfg(A[k, k], A[k + 1:, k])
+        vf = np.concatenate([np.ones(1, dtype=A.dtype), v])
+        A[k, k] = beta
+        A[k + 1:, k] = v
+        if k + 1 < n:
+            w = vf.conj() @ A[k:, k + 1:]
+            A[k:, k + 1:] -= np.conj(tau) * np.outer(vf, w)
+        taus.append(tau)
+        betas.append(beta)
+        vs.append(vf)
     Q = np.zeros((m, n), dtype=A.dtype)
     Q[np.arange(n), np.arange(n)] = 1.0
     for k in reversed(range(n)):
-        v = vs[k]
-        if v is None:
-            continue
-        Q[k:, :] -= 2.0 * np.outer(v, v.conj() @ Q[k:, :])
-    # make diag(R) positive real: R = Q^H X; scale columns of Q by phase of diag(R)
-    d = np.einsum("ij,ij->j", Q.conj(), X)
-    ph = np.where(d != 0, d / np.abs(d), 1.0)
-    return Q * ph[None, :]
+        vf = vs[k]
+        Q[k:, :] -= taus[k] * np.outer(vf, vf.conj() @ Q[k:, :])
+    return Q, np.array(betas)
+
+
+def householder_qr(X: np.ndarray) -> np.ndarray:
+    """Alg.4 l.9 "X <- ScaLAPACK-HHQR(X, comm)": the thin Q of householder_factor with
+    column k scaled by sign(beta_k) (+1 for beta_k = 0), so diag(R) is non-negative real and Q
+    equals CholeskyQR's Q for full-rank X (reading #33).  Also a CholeskyQR pin."""
+    Q, beta = householder_factor(X)
+    sgn = np.where(beta < 0.0, -1.0, 1.0)
+    return Q * sgn[None, :]

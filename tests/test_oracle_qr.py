@@ -68,13 +68,41 @@ def test_trsm_matches_lapack(complex_):
 
 
 @pytest.mark.parametrize("complex_", [True, False])
-def test_householder_matches_lapack(complex_):
+@pytest.mark.parametrize("zero_col", [None, 4, 0, 19])
+def test_householder_matches_lapack(complex_, zero_col):
+    """householder_factor is xGEQR2 + xUNG2R: the same reflectors as LAPACK xGEQRF + xUNGQR
+    (numpy.linalg.qr), so Q and diag(R) agree to rounding even for a rank-deficient X (an exact
+    zero column), where Q is not determined by X alone."""
     X = ci.svd_synthesized(70, 20, 1e4, 5, complex_)
-    Q = oracle.householder_qr(X)
+    if zero_col is not None:
+        X[:, zero_col] = 0
+    Qf, beta = oracle.householder_factor(X)
     Ql, Rl = np.linalg.qr(X)
-    ph = np.diag(Rl) / np.abs(np.diag(Rl))
-    assert np.allclose(Q, Ql * ph[None, :], rtol=0, atol=1e-12)
+    assert np.abs(Qf - Ql).max() <= 10 * 1e4 * 2.0 ** -53     # kappa u (different blocking)
+    assert np.abs(beta - np.diag(Rl).real).max() <= 1e-12 * np.abs(X).max()
+    assert np.abs(np.diag(Rl).imag).max() == 0.0
+    Q = oracle.householder_qr(X)
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(20)) <= 1e-13
+    R = Q.conj().T @ X                                     # upper, non-negative real diagonal
+    assert np.abs(np.tril(R, -1)).max() <= 1e-13 * np.abs(X).max()
+    assert (np.diag(R).real >= -1e-13).all() and np.abs(np.diag(R).imag).max() <= 1e-13
+    if zero_col is None:
+        ph = np.diag(Rl) / np.abs(np.diag(Rl))
+        assert np.allclose(Q, Ql * ph[None, :], rtol=0, atol=1e-12)
+
+
+def test_larfg_definition():
+    """H^H (alpha; x) = (beta; 0) with H = I - tau v v^H, v = (1; v'), beta real; |beta| = norm."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(9) + 1j * rng.standard_normal(9)
+    tau, beta, v = oracle.larfg(x[0], x[1:])
+    vf = np.concatenate([[1.0], v])
+    H = np.eye(9) - tau * np.outer(vf, vf.conj())
+    y = H.conj().T @ x
+    assert abs(y[0] - beta) <= 1e-14 * np.linalg.norm(x) and np.abs(y[1:]).max() <= 1e-14 * 4
+    assert abs(abs(beta) - np.linalg.norm(x)) <= 1e-14 * np.linalg.norm(x)
+    assert np.abs(H.conj().T @ H - np.eye(9)).max() <= 1e-14      # unitary
+    assert oracle.larfg(2.5, np.zeros(3))[0] == 0.0                 # H = I
 
 
 def test_shift_golden(golden):
@@ -174,3 +202,25 @@ def test_degree36_plain_cqr2_fails_and_escalates():
     assert info > 0 and passes == 0
     res = oracle.caqr(X, 1e3)                   # force CQR2: first POTRF fails -> shifted
     assert res["status"] == 0 and res["variant"] == oqr.SHIFTED and res["passes"] == 3
+
+
+def test_hhqr_fallback_paths():
+    """Alg.4 l.8-9 and reading #33.  (a) X = 0: norm = 0 so s = 0 and the shifted
+    POTRF fails at pivot 1 -> HHQR, whose reflectors are all identities: Q = [I; 0].
+    (b) an exact zero column j: CQR2's first POTRF fails at j+1 (escalation, reading #14), the
+    shifted pass succeeds and keeps column j exactly zero, the next POTRF fails at j+1 -> HHQR
+    on that output: orthonormal Q spanning X, Q^H X upper triangular."""
+    Z = np.zeros((40, 6), dtype=np.complex128)
+    res = oracle.caqr(Z, 1e9)
+    assert (res["status"], res["variant"], res["passes"], res["info"]) == (0, oqr.HOUSEHOLDER, 0, 1)
+    assert np.array_equal(res["Q"], np.eye(40, 6))
+    X = ci.svd_synthesized(300, 10, 10.0, 3, True)
+    X[:, 4] = 0
+    for est in (1e3, 1e9):
+        res = oracle.caqr(X, est)
+        assert (res["status"], res["variant"], res["passes"], res["info"]) == (0, oqr.HOUSEHOLDER, 1, 5)
+        Q = res["Q"]
+        assert np.linalg.norm(Q.conj().T @ Q - np.eye(10)) <= 1e-13
+        R = Q.conj().T @ X
+        assert np.abs(np.tril(R, -1)).max() <= 1e-13 * np.abs(X).max()
+        assert np.linalg.norm(Q @ R - X) <= 1e-13 * np.linalg.norm(X)
