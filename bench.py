@@ -333,7 +333,7 @@ def main():
     launches_per_filter = int(np.max(degrees))
     hemm_avg_ms = hemm_ms / (args.steps * launches_per_filter)
     hemm_achieved = per_gpu_hemm_flops / launches_per_filter / (hemm_avg_ms / 1e3) / 1e12
-    gpu_launches = int(sum(prof_n[k] for k in ("hemm", "gram", "potrf", "trsm", "other")))
+    gpu_launches = int(sum(prof_n[k] for k in ("hemm", "gram", "potrf", "trsm", "other", "hhqr")))
 
     # ---- NEXT-2: Rayleigh-Ritz (Alg.2 l.16-22) on the step's orthonormal output, timed once
     barrier()
@@ -359,6 +359,27 @@ def main():
                      "tflops": (8.0 if w["complex_"] else 2.0) * float(N) ** 2 * n / (res_ms / 1e3) / 1e12,
                      "max_resid": float(np.max(resid)),
                      "note": "chase_residuals on the step output (NEXT-1, Alg.2 l.23-28), not part of the step"}
+
+    # ---- CholeskyQR (Alg.4) vs Householder QR (Alg.4 l.9 fallback / the HHQR mode of P:448,
+    # Table 3) on the same filtered block, each timed once after a warm-up
+    V_t.copy_(V0_host)
+    h.filter(A_local, V, degrees, b.c, b.e, bounds)
+    Xf_t = V_t.clone()
+    qr_cmp = {}
+    for name, fn in (("cholqr", lambda: h.cholqr(V, est)), ("hhqr", lambda: h.hhqr(V))):
+        V_t.copy_(Xf_t)
+        fn()                                           # warm-up
+        V_t.copy_(Xf_t)
+        barrier()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        barrier()
+        qr_cmp[name + "_ms"] = allmax(e0.elapsed_time(e1))
+    del Xf_t
+    qr_cmp["cholqr_speedup_over_hhqr"] = qr_cmp["hhqr_ms"] / qr_cmp["cholqr_ms"]
+    qr_cmp["note"] = ("same filtered block; paper Table 3 (P:455-483) compares ChASE with HHQR "
+                      "(ScaLAPACK, CPU) against CholeskyQR; here both run on the GPU")
 
     # ---- end-to-end through the public API with host buffers (V in from pinned host, V out)
     e2e = None
@@ -426,10 +447,11 @@ def main():
                                         "MEASURED_PEAKS.json has no FP64 entry",
                          "per_launch_flops": per_gpu_hemm_flops / launches_per_filter,
                          "avg_launch_ms": hemm_avg_ms},
-            "profile_ms_per_step": {k: v / args.steps for k, v in prof_ms.items() if k != "reserved"},
+            "profile_ms_per_step": {k: v / args.steps for k, v in prof_ms.items()},
             "gpu_launches": gpu_launches,
             "residuals": residual_info,
             "rayleigh_ritz": rr_info,
+            "qr_vs_hhqr": qr_cmp,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

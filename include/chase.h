@@ -3,7 +3,7 @@
  * the 2D-distributed Chebyshev polynomial filter and the condition-driven CholeskyQR family.
  *
  * Citations: P:NNN = /root/reference/PAPER.md line, S:NNN = SPEC.md line; "Alg.k l.m" = line m
- * of Algorithm k as printed.  Readings of silent/garbled passages are numbered #1..#24 in
+ * of Algorithm k as printed.  Readings of silent/garbled passages are numbered #1..#33 in
  * DESIGN.md ("Readings").
  *
  * Conventions shared by every entry point
@@ -45,8 +45,14 @@ typedef enum {
 typedef enum { CHASE_R64 = 1, CHASE_C128 = 2 } chase_dtype_t;
 
 /* QR variants of Alg.4.  CHOL1 = CholeskyQR (cholDegree 1), CHOL2 = CholeskyQR2,
- * SHIFTED = one shifted pass (POTRF(G + sI)) followed by CholeskyQR2 (reading #13). */
-typedef enum { CHASE_QR_CHOL1 = 1, CHASE_QR_CHOL2 = 2, CHASE_QR_SHIFTED = 3 } chase_qr_variant_t;
+ * SHIFTED = one shifted pass (POTRF(G + sI)) followed by CholeskyQR2 (reading #13),
+ * HOUSEHOLDER = the HHQR fallback of Alg.4 l.9 / the HHQR mode of P:448. */
+typedef enum {
+  CHASE_QR_CHOL1 = 1,
+  CHASE_QR_CHOL2 = 2,
+  CHASE_QR_SHIFTED = 3,
+  CHASE_QR_HOUSEHOLDER = 4
+} chase_qr_variant_t;
 
 /* Spectral bounds of Alg.1 l.2: mu_1 ~ lambda_min, mu_ne ~ lambda_{nev+nex},
  * b_sup >= lambda_max.  The filter uses mu_1 for the scaling point (reading #2); c and e are
@@ -222,20 +228,40 @@ chase_status_t chase_filter_schedule(int64_t N, int p, int q, int myrow, int myc
  * then AllReduce SUM over ccomm), [shifted pass: norm = ||V||_F^2 = Re tr(G) (reading #12),
  * s = 11(N*ncols + ncols(ncols+1)) u norm, u = 2^-53, G += sI], G = R^H R (POTRF, R upper
  * with positive real diagonal), V = V R^{-1} (TRSM).  If the first POTRF of CholeskyQR or
- * CholeskyQR2 fails (V untouched) the call escalates to the shifted path (reading #14).
+ * CholeskyQR2 fails (V untouched) the call escalates to the shifted path (reading #14).  If
+ * the shifted POTRF fails, the call reverts to Householder QR (Alg.4 l.8-9), and
+ * so does any later POTRF failure, on the V of the last successful pass (reading #33); with
+ * chase_set_qr_mode(h, 1) every call runs Householder QR (the HHQR mode of P:448).
  *
  *  V        device, in/out: the C-layout block as for chase_filter, ldv >= n_r (16-byte
  *           pitch as for chase_filter).
  *  ncols    1..n_max columns to orthonormalise (all given columns; reading #16).
  *  cond_est >= 1, e.g. from chase_cond_est (Alg.5).
- *  stats    host, nullable: qr_variant (executed branch) and qr_passes.
- *  info     host, nullable: 0, or the 1-based failing pivot of the last POTRF.
+ *  stats    host, nullable: qr_variant (executed branch, CHASE_QR_HOUSEHOLDER when the
+ *           fallback ran) and qr_passes (successful Cholesky passes).
+ *  info     host, nullable: 0, or the 1-based failing pivot of the last failed POTRF.
  * Synchronises the stream once per POTRF (4-byte info read).
- * Errors: CHASE_EINVAL (bad sizes, cond_est < 1 or NaN), CHASE_ECHOL (shifted POTRF failed;
- * the caller decides on Householder QR, P:299 -- out of scope here), CHASE_ESTATE,
- * CHASE_ECUDA, CHASE_ENCCL. */
+ * Errors: CHASE_EINVAL (bad sizes, cond_est < 1 or NaN), CHASE_ESTATE, CHASE_ECUDA,
+ * CHASE_ENCCL.  (CHASE_ECHOL is no longer returned: Householder QR always succeeds.) */
 chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols, double cond_est,
                             chase_stats_t* stats, int32_t* info);
+
+/* ---------------------------------------------------------------------------------------
+ * Householder QR -- Alg.4 l.9 "X <- ScaLAPACK-HHQR(X, comm)" on the GPU:
+ * blocked Householder QR of the C-layout block over the rows of the column communicator
+ * (xGEQRF order, 32-wide panels as the paper's ScaLAPACK column block; reflectors of
+ * LAPACK xLARFG; compact-WY trailing updates on the tensor-core GEMMs; AllReduce over ccomm
+ * per column and per panel), then the thin Q (xUNGQR order), written back into V with column
+ * j scaled by sign(R_jj) so diag(R) is non-negative (reading #33).  Never fails on rank
+ * deficiency (H_j = I for a zero column).  Collective over the grid (identical ncols).
+ *  V, ldv, ncols as for chase_cholqr.  Uses the W workspace for Q.
+ * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL. */
+chase_status_t chase_hhqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols);
+
+/* QR mode of chase_cholqr (and hence chase_solve): 0 = Alg.4 dispatch (default), 1 = Householder
+ * QR in every call (the "ChASE with HHQR" configuration of P:448, Table 3).  Host only.
+ * Errors: CHASE_EINVAL (mode not 0/1). */
+chase_status_t chase_set_qr_mode(chase_handle_t h, int32_t mode);
 
 /* ---------------------------------------------------------------------------------------
  * The full ChASE iteration -- Alg.2 for the nev lowest eigenpairs:
@@ -310,7 +336,8 @@ double chase_shift_value(int64_t m, int64_t n, double norm);
  * handle's stream; chase_profile_read synchronises, returns per-category device time (ms)
  * and kernel-launch counts since the last read, and resets.  Categories (arrays of 8):
  *   0 HEMM odd steps (A^H C -> B)   1 HEMM even steps (A B -> C)   2 AllReduce (NCCL calls)
- *   3 Gram   4 POTRF   5 TRSM   6 other kernels   7 reserved (0) */
+ *   3 Gram   4 POTRF   5 TRSM   6 other kernels   7 Householder QR (whole call; launches
+ *   counted there, its GEMMs included) */
 chase_status_t chase_profile_enable(chase_handle_t h, int enable);
 chase_status_t chase_profile_read(chase_handle_t h, double ms[8], int64_t launches[8]);
 

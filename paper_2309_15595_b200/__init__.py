@@ -21,11 +21,11 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CHASE_LIB") or os.path.join(_PKG, "libchase.so")   # CHASE_LIB: A/B builds
 
 CHASE_R64, CHASE_C128 = 1, 2
-CHASE_QR_CHOL1, CHASE_QR_CHOL2, CHASE_QR_SHIFTED = 1, 2, 3
+CHASE_QR_CHOL1, CHASE_QR_CHOL2, CHASE_QR_SHIFTED, CHASE_QR_HOUSEHOLDER = 1, 2, 3, 4
 STATUS = {0: "CHASE_OK", 1: "CHASE_EINVAL", 2: "CHASE_EDEGREE", 3: "CHASE_EBOUNDS",
           4: "CHASE_ECHOL", 5: "CHASE_ECUDA", 6: "CHASE_ENCCL", 7: "CHASE_ENOMEM",
           8: "CHASE_ESTATE", 9: "CHASE_ENOCONV"}
-PROFILE_CATEGORIES = ("hemm_odd", "hemm_even", "allreduce", "gram", "potrf", "trsm", "other", "reserved")
+PROFILE_CATEGORIES = ("hemm_odd", "hemm_even", "allreduce", "gram", "potrf", "trsm", "other", "hhqr")
 
 # every symbol include/chase.h declares (checked by tests/test_abi.py)
 EXPORTED = (
@@ -35,7 +35,8 @@ EXPORTED = (
     "chase_shift_value", "chase_profile_enable", "chase_profile_read", "chase_destroy",
     "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
     "chase_set_fused_workspace", "chase_create_cyclic", "chase_local_indices",
-    "chase_cyclic_indices", "chase_rayleigh_ritz", "chase_solve",
+    "chase_cyclic_indices", "chase_rayleigh_ritz", "chase_solve", "chase_hhqr",
+    "chase_set_qr_mode",
 )
 
 
@@ -97,6 +98,8 @@ def load() -> ctypes.CDLL:
         "chase_filter_schedule": (I32, [I64, I32, I32, I32, I32, I64, ctypes.POINTER(I32), I32,
                                         ctypes.POINTER(chase_step_record_t), ctypes.POINTER(I32), c_i64p]),
         "chase_cholqr": (I32, [V, V, I64, I64, D, ctypes.POINTER(chase_stats_t), ctypes.POINTER(I32)]),
+        "chase_hhqr": (I32, [V, V, I64, I64]),
+        "chase_set_qr_mode": (I32, [V, I32]),
         "chase_cond_est": (D, [ctypes.POINTER(D), I64, D, D, ctypes.POINTER(I32), I64]),
         "chase_residuals": (I32, [V, V, I64, V, I64, I64, ctypes.POINTER(D), ctypes.POINTER(D)]),
         "chase_fused_workspace_size": (I32, [V, ctypes.POINTER(ctypes.c_size_t)]),
@@ -290,6 +293,18 @@ def chase_cholqr(h, V, cond_est: float, ncols: int | None = None, raise_on_error
     return {"status": s, "variant": st.qr_variant, "passes": st.qr_passes, "info": info.value}
 
 
+def chase_hhqr(h, V, ncols: int | None = None):
+    """Householder QR (Alg.4 l.9) in place on V: V <- Q with diag(R) >= 0."""
+    v_ptr, ldv = _colmajor(V, "V")
+    ncols = V.shape[1] if ncols is None else ncols
+    _check(load().chase_hhqr(h, v_ptr, ldv, ncols), "chase_hhqr")
+
+
+def chase_set_qr_mode(h, mode: int):
+    """0: Alg.4 dispatch; 1: Householder QR in every chase_cholqr call."""
+    _check(load().chase_set_qr_mode(h, int(mode)), "chase_set_qr_mode")
+
+
 def chase_residuals(h, A_local, V, ritz, ncols: int | None = None):
     """Residual norms ||A v_j - ritz_j v_j|| (Alg.2 l.23-28) of the columns of V."""
     a_ptr, lda = _colmajor(A_local, "A_local")
@@ -399,6 +414,12 @@ class Chase:
 
     def cholqr(self, V, cond_est, ncols=None, raise_on_error=True):
         return chase_cholqr(self.h, V, cond_est, ncols, raise_on_error)
+
+    def hhqr(self, V, ncols=None):
+        return chase_hhqr(self.h, V, ncols)
+
+    def set_qr_mode(self, mode):
+        return chase_set_qr_mode(self.h, mode)
 
     def solve(self, A_local, V, nev, nex, **kw):
         return chase_solve(self.h, A_local, V, nev, nex, **kw)

@@ -16,6 +16,7 @@
 #include "chase.h"
 #include "dgemm.cuh"
 #include "eig.cuh"
+#include "hhqr.cuh"
 #include "qr_kernels.cuh"
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
@@ -103,7 +104,8 @@ static void block_part(int64_t N, int P, int k, int64_t* size, int64_t* start) {
 }
 
 // ==================================================================== handle
-enum { CAT_HEMM_ODD = 0, CAT_HEMM_EVEN, CAT_ALLREDUCE, CAT_GRAM, CAT_POTRF, CAT_TRSM, CAT_OTHER, CAT_N };
+enum { CAT_HEMM_ODD = 0, CAT_HEMM_EVEN, CAT_ALLREDUCE, CAT_GRAM, CAT_POTRF, CAT_TRSM, CAT_OTHER,
+       CAT_HHQR, CAT_N };
 
 struct chase_handle_s {
   chase_dtype_t dt;
@@ -111,6 +113,9 @@ struct chase_handle_s {
   int p, q, myrow, mycol;
   int64_t n_r, n_c, r0, c0;       // r0 = c0 = -1 for the block-cyclic distribution
   int64_t nb = 0;                 // block-cyclic block size (0 = block distribution)
+  int64_t voff = 0;               // first "virtual" row of this rank in the column communicator
+                                  //   (rank 0's rows, rank 1's, ...): the HHQR row order
+  int qr_mode = 0;                // 0: Alg.4 dispatch; 1: Householder QR always (Table 3)
   std::vector<int64_t> rows_g, cols_g;   // global indices of the local rows / columns
   int* d_band_odd = nullptr;      // block-cyclic: B-layout row -> C-layout row of the diagonal
   int* d_band_even = nullptr;     //   C-layout row -> B-layout row of the diagonal (or -1)
@@ -131,6 +136,7 @@ struct chase_handle_s {
   char* eigws = nullptr;    // Jacobi eigensolver region (see eig_bytes)
   char* c2ws = nullptr;     // solver: C2
   char* lanws = nullptr;    // solver: Lanczos basis
+  char* hhws = nullptr;     // Householder QR fallback (see hh_layout)
   double* d_ritz = nullptr;
   double* d_nrm = nullptr;
   int* d_info = nullptr;
@@ -198,7 +204,7 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, hh, info, s, total;
 };
 constexpr int LANCZOS_K = 25;       // Lanczos steps per run (bounds, Alg.1 l.2)
 constexpr int LANCZOS_RUNS = 4;     // independent runs pooled for the DoS estimate
@@ -211,6 +217,34 @@ static size_t eig_bytes(int64_t n_max) {
          align256(np * sizeof(int)) + align256((size_t)(L + 1) * L * sizeof(int)) +
          align256(2 * JAC_RED_BLOCKS * sizeof(double) + 2 * sizeof(double));
 }
+// Householder QR scratch: panel reflectors Vp (n_r x 128), the compact-WY factors T of every
+// panel (128 x n_max), two 128 x n_max products, S = Vp^H Vp, tau, beta, CTA partials, split-K
+// partial products, reduced scalars and the arrival counters.
+struct HhLayout {
+  size_t vp, t, wb, wb2, s, tau, beta, part, psplit, red_n, red_w, ctr, total;
+  int64_t split_cols;     // columns of HH_NB-row split-K partials the psplit buffer holds
+};
+static HhLayout hh_layout(const chase_handle_s* h) {
+  const size_t es = esize_of(h->dt);
+  HhLayout L;
+  size_t off = 0;
+  L.vp = off;   off += align256((size_t)pad_ld(h->n_r) * HH_NB * es);
+  L.t = off;    off += align256((size_t)HH_NB * (h->n_max + HH_NB) * es);
+  L.wb = off;   off += align256((size_t)HH_NB * h->n_max * es);
+  L.wb2 = off;  off += align256((size_t)HH_NB * h->n_max * es);
+  L.s = off;    off += align256((size_t)HH_NB * HH_NB * es);
+  L.tau = off;  off += align256((size_t)h->n_max * es);
+  L.beta = off; off += align256((size_t)h->n_max * sizeof(double));
+  L.part = off; off += align256((size_t)(HH_NCH + 1) * HH_GRID_MAX * HH_CH * 16);
+  L.split_cols = std::max<int64_t>(h->n_max, std::min<int64_t>(2 * 148 * 64, 64 * h->n_max));
+  L.psplit = off; off += align256((size_t)HH_NB * L.split_cols * es);
+  L.red_n = off; off += 256;
+  L.red_w = off; off += align256((size_t)HH_NB * 16);
+  L.ctr = off;  off += 256;
+  L.total = off;
+  return L;
+}
+
 // B-layout block (n_c x n_max) | Gram/R (n_max x n_max) | TRSM output W (n_r x n_max)
 // | inverted diagonal blocks of R (64 x n_max) | info | shift
 static WsLayout ws_layout(const chase_handle_s* h) {
@@ -239,6 +273,8 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)pad_ld(h->n_r) * h->n_max * es);
   L.lan = off;                                          // solver: Lanczos basis + scalars
   off += align256((size_t)pad_ld(h->n_r) * (LANCZOS_K + 2) * es) + 4096;
+  L.hh = off;                                           // Householder QR fallback
+  off += hh_layout(h).total;
   L.info = off;
   off += 256;
   L.s = off;
@@ -256,7 +292,7 @@ static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B swi
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM));
+  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM) * std::max(1, a.k_split));
   if (conj) {
     if (!g_attr_done[1][0]) {
       CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -283,7 +319,7 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM));
+  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM) * std::max(1, a.k_split));
   if (trans) {
     if (!g_attr_done[1][1]) {
       CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -323,6 +359,8 @@ struct GemmReq {
   const double* col_shift;   // residual epilogue (Alg.2 l.25): out -= col_shift[n] y2(m, n)
   const void* y2;
   int64_t ldy2;
+  int k_split;               // split-K copies (> 1: partial products at out + s * split_ld)
+  int64_t split_ld;
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
@@ -339,6 +377,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.diag_k = r.diag_k;
     a.a3d = r.a3d;
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
+    a.k_split = r.k_split; a.split_ld = r.split_ld;
     return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
   }
   DGemmArgs a;
@@ -353,6 +392,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.diag_k = r.diag_k;
   a.a3d = r.a3d;
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
+  a.k_split = r.k_split; a.split_ld = r.split_ld;
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
 }
 
@@ -624,6 +664,7 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
   if (nb == 0) {
     block_part(N, p, myrow, &h->n_r, &h->r0);
     block_part(N, q, mycol, &h->n_c, &h->c0);
+    h->voff = h->r0;
     for (int64_t l = 0; l < h->n_r; ++l) h->rows_g.push_back(h->r0 + l);
     for (int64_t l = 0; l < h->n_c; ++l) h->cols_g.push_back(h->c0 + l);
   } else {
@@ -635,6 +676,11 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
     if (h->n_r == 0 || h->n_c == 0) {
       delete h;
       return CHASE_EINVAL;                    // every grid row/column must own at least one block
+    }
+    std::vector<int64_t> other;
+    for (int i2 = 0; i2 < myrow; ++i2) {
+      cyclic_indices(N, p, i2, nb, &other);
+      h->voff += (int64_t)other.size();
     }
   }
   h->device = device;
@@ -714,6 +760,7 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->eigws = base + L.eig;
   h->c2ws = base + L.c2;
   h->lanws = base + L.lan;
+  h->hhws = base + L.hh;
   h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
   h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
   if (h->nb > 0) {
@@ -1159,6 +1206,8 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
 
 bool g_qr_attr_done = false;
 
+#include "hhqr.inc"
+
 }  // namespace
 
 extern "C" {
@@ -1194,19 +1243,21 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   int variant = cond_est > 1e8 ? CHASE_QR_SHIFTED : (cond_est < 20.0 ? CHASE_QR_CHOL1 : CHASE_QR_CHOL2);
   int info = 0, passes = 0;
   chase_status_t st = CHASE_OK;
-  if (variant != CHASE_QR_SHIFTED) {
+  bool hh = h->qr_mode == 1;                     // HHQR in every call (Table 3)
+  if (!hh && variant != CHASE_QR_SHIFTED) {
     const int rounds = variant == CHASE_QR_CHOL1 ? 1 : 2;
     for (int i = 0; i < rounds; ++i) {
       st = cholqr_pass(h, V, ldv, n, false, mp, &info);
       if (st != CHASE_OK) break;
       ++passes;
     }
-    if (st == CHASE_ECHOL && passes == 0) {     // reading #14: escalate, V untouched
-      variant = CHASE_QR_SHIFTED;
+    if (st == CHASE_ECHOL) {
+      if (passes == 0) variant = CHASE_QR_SHIFTED;   // reading #14: escalate, V untouched
+      else hh = true;                                // reading #33: HHQR on the current V
       st = CHASE_OK;
     }
   }
-  if (variant == CHASE_QR_SHIFTED && st == CHASE_OK && passes == 0) {
+  if (!hh && variant == CHASE_QR_SHIFTED && st == CHASE_OK && passes == 0) {
     st = cholqr_pass(h, V, ldv, n, true, mp, &info);
     if (st == CHASE_OK) {
       ++passes;
@@ -1215,6 +1266,14 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
         if (st == CHASE_OK) ++passes;
       }
     }
+    if (st == CHASE_ECHOL) {                        // Alg.4 l.8-9; reading #33
+      hh = true;
+      st = CHASE_OK;
+    }
+  }
+  if (hh && st == CHASE_OK) {
+    variant = CHASE_QR_HOUSEHOLDER;
+    st = hhqr_run(h, V, ldv, n);
   }
   if (stats) {
     stats->qr_variant = variant;
@@ -1222,6 +1281,21 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   }
   if (info_out) *info_out = info;
   return st;
+}
+
+chase_status_t chase_hhqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols) {
+  if (!h || !V) return CHASE_EINVAL;
+  if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
+  if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;
+  if (reinterpret_cast<uintptr_t>(V) & 15) return CHASE_EINVAL;
+  if (!h->ws) return CHASE_ESTATE;
+  return hhqr_run(h, V, ldv, (int)ncols);
+}
+
+chase_status_t chase_set_qr_mode(chase_handle_t h, int32_t mode) {
+  if (!h || (mode != 0 && mode != 1)) return CHASE_EINVAL;
+  h->qr_mode = mode;
+  return CHASE_OK;
 }
 
 // Alg.2 l.16 / l.23 "B2 <- Bcast(C2, ccomm)": the rows [c0, c0+n_c) (block-cyclic: the column

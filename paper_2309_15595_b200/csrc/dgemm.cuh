@@ -57,6 +57,8 @@ struct DGemmArgs {
   const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (Alg.2 l.25)
   const double* y2;
   long long ldy2;
+  int k_split;             // split-K: see zgemm.cuh
+  long long split_ld;
 };
 
 __device__ __forceinline__ int dg_kperm(int t, int h) {
@@ -78,15 +80,21 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   // grouped rasterisation (1D grid): consecutive CTAs walk DG_GROUP_M m-tiles, then the next
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
-  const int group = blockIdx.x / (DG_GROUP_M * n_tiles);
+  // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
+  const int split = g.k_split > 1 ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
+  const int bid = (int)blockIdx.x - split * n_tiles * m_tiles;
+  const int group = bid / (DG_GROUP_M * n_tiles);
   const int first_m = group * DG_GROUP_M;
   const int gm = min(DG_GROUP_M, m_tiles - first_m);
-  const int within = blockIdx.x - group * DG_GROUP_M * n_tiles;
+  const int within = bid - group * DG_GROUP_M * n_tiles;
   const int m0 = (first_m + within % gm) * DG_BM, n0 = (within / gm) * DG_BN;
   if (g.upper_only && m0 > n0 + DG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int KT = (g.K + DG_BK - 1) / DG_BK;
-  const int dk = g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0);   // per-CTA k offset
+  const int KT_all = (g.K + DG_BK - 1) / DG_BK;
+  const int KTc = g.k_split > 1 ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
+  const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
+  const int kbase = split * KTc * DG_BK;
+  const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < DG_STAGES; ++s) {
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       const int n = wn * DG_WN + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
     }
-    if (kt * DG_BK + k >= g.K) {
+    if (kbase + kt * DG_BK + k >= g.K) {
 #pragma unroll
       for (int mt = 0; mt < DG_MT; ++mt) f.a[mt][0] = f.a[mt][1] = 0.0;
 #pragma unroll
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
           if (bsrc >= 0) v -= g.c * g.xin[(long long)bsrc + (long long)col * g.ldx];
           if (g.col_shift != nullptr) v -= g.col_shift[col] * g.y2[(long long)row + (long long)col * g.ldy2];
           v *= g.alpha;
-          double* o = g.out + (long long)row + (long long)col * g.ldo;
+          double* o = g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) v += g.beta * *o;
           *o = v;
         }

@@ -75,6 +75,8 @@ struct ZGemmArgs {
   const double* col_shift; // non-null: out -= col_shift[n] * y2(m, n) before alpha (residual,
   const double2* y2;       //   Alg.2 l.25 "B <- B - ritzv B2" fused into the HEMM epilogue)
   long long ldy2;
+  int k_split;             // > 1: split-K -- CTA blockIdx / tiles takes k-tiles [s KTc, (s+1) KTc)
+  long long split_ld;      //   and writes its partial product to out + s * split_ld (no beta)
 };
 
 template <bool CONJ>
@@ -92,15 +94,21 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // grouped rasterisation (1D grid): consecutive CTAs walk ZG_GROUP_M m-tiles, then the next
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
-  const int group = blockIdx.x / (ZG_GROUP_M * n_tiles);
+  // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
+  const int split = g.k_split > 1 ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
+  const int bid = (int)blockIdx.x - split * n_tiles * m_tiles;
+  const int group = bid / (ZG_GROUP_M * n_tiles);
   const int first_m = group * ZG_GROUP_M;
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
-  const int within = blockIdx.x - group * ZG_GROUP_M * n_tiles;
+  const int within = bid - group * ZG_GROUP_M * n_tiles;
   const int m0 = (first_m + within % gm) * ZG_BM, n0 = (within / gm) * ZG_BN;
   if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int KT = (g.K + ZG_BK - 1) / ZG_BK;
-  const int dk = g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0);   // per-CTA k offset
+  const int KT_all = (g.K + ZG_BK - 1) / ZG_BK;
+  const int KTc = g.k_split > 1 ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
+  const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
+  const int kbase = split * KTc * ZG_BK;
+  const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ZG_STAGES; ++s) {
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       const int n = wn * ZG_WN + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
     }
-    if (kt * ZG_BK + 8 * u + k >= g.K) {               // K tail (the TMA box may hold stale data)
+    if (kbase + kt * ZG_BK + 8 * u + k >= g.K) {               // K tail (the TMA box may hold stale data)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) f.a[mt][0] = f.a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           }
           vr *= g.alpha;
           vi *= g.alpha;
-          double2* o = g.out + (long long)row + (long long)col * g.ldo;
+          double2* o = g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) {
             const double2 old = *o;
             vr += g.beta * old.x;

@@ -1,6 +1,6 @@
 """torchrun worker for tests/test_gpu_multi.py: one rank per GPU, p x q grid, NCCL (or fused
-peer-memory reduction).  Runs chase_filter (twice: bitwise repeat check), chase_cholqr and
-chase_residuals through the C-ABI on a seeded problem and writes the gathered result to
+peer-memory reduction).  Runs chase_filter (twice: bitwise repeat check), chase_cholqr, chase_hhqr,
+chase_residuals, chase_rayleigh_ritz through the C-ABI on a seeded problem and writes the gathered result to
 <out>.npz on rank 0.
 argv: p q N c|r out [pad] [nccl|fused] [nb]"""
 import os
@@ -59,6 +59,11 @@ def main():
     rec, mv = h.record()
     Vf = Vd.T.cpu().numpy().T.copy()
     est = cb.chase_cond_est(lam, b.c, b.e, degs, 0)
+    # Householder QR (Alg.4 l.9 fallback) of the filtered block over the column comm
+    Vh = dev(Vf)
+    h.hhqr(Vh)
+    torch.cuda.synchronize()
+    Hq = Vh.T.cpu().numpy().T.copy()
     qr = h.cholqr(Vd, est, raise_on_error=False)
     torch.cuda.synchronize()
     Q = Vd.T.cpu().numpy().T.copy()
@@ -79,27 +84,30 @@ def main():
     Xr = Vd.T.cpu().numpy().T.copy()
     g = [None] * world
     dist.all_gather_object(g, (rank, myrow, mycol, rows, n_r, n_c, Vf, Q, rec, mv, qr, resid, ritz, repeat_equal,
-                               theta, Xr))
+                               theta, Xr, Hq))
     if rank == 0:
         Vfull = np.zeros((N, n), dtype=dt)
         Qfull = np.zeros((N, n), dtype=dt)
         Xfull = np.zeros((N, n), dtype=dt)
+        Hfull = np.zeros((N, n), dtype=dt)
         replica = 0.0
         for x in g:
             if x[2] == 0:
                 Vfull[x[3]] = x[6]
                 Qfull[x[3]] = x[7]
                 Xfull[x[3]] = x[15]
+                Hfull[x[3]] = x[16]
         for x in g:
             replica = max(replica, float(np.max(np.abs(x[6] - Vfull[x[3]]))),
                           float(np.max(np.abs(x[7] - Qfull[x[3]]))),
-                          float(np.max(np.abs(x[15] - Xfull[x[3]]))))
+                          float(np.max(np.abs(x[15] - Xfull[x[3]]))),
+                          float(np.max(np.abs(x[16] - Hfull[x[3]]))))
         np.savez(out, V=Vfull, Q=Qfull, replica=replica, est=est,
                  variants=np.array([x[10]["variant"] for x in g]), passes=np.array([x[10]["passes"] for x in g]),
                  status=np.array([x[10]["status"] for x in g]), mv=np.array([x[9] for x in g]),
                  recs=np.array([str(x[8]) for x in g]), ranks=np.array([[x[1], x[2], x[4], x[5]] for x in g]),
                  resid=np.array([x[11] for x in g]), ritz=g[0][12],
-                 repeat_equal=np.array([x[13] for x in g]), X=Xfull,
+                 repeat_equal=np.array([x[13] for x in g]), X=Xfull, H=Hfull,
                  theta=np.array([x[14] for x in g]))
     h.close()
     dist.destroy_process_group()

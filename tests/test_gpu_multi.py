@@ -93,6 +93,10 @@ def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode, nb):
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(n)) <= 1e-12
     kappa = np.linalg.cond(ref)
     assert np.linalg.norm(Q - qref["Q"]) / np.sqrt(n) <= 100 * kappa * 2.0 ** -53 + 1e-13
+    # Householder QR (Alg.4 l.9) over the column communicator: the oracle's HHQR Q
+    Hq = res["H"]
+    assert np.linalg.norm(Hq.conj().T @ Hq - np.eye(n)) <= 1e-12
+    assert np.linalg.norm(Hq - oracle.householder_qr(ref)) / np.sqrt(n) <= 100 * kappa * 2.0 ** -53 + 1e-13
     # residuals (Alg.2 l.23-28): identical on every rank, equal to the oracle on the gathered Q
     rres = oracle.residuals(A, Q, res["ritz"])
     assert np.all(res["resid"] == res["resid"][0])
