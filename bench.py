@@ -264,7 +264,7 @@ def main():
     comm_mode = "none"
     if world > 1:
         comm_mode = "nccl"
-        if args.comm == "fused" and w["complex_"]:
+        if args.comm == "fused":
             from paper_2309_15595_b200 import dist as cdist
             try:
                 cdist.enable_fused_comm(h)
@@ -381,23 +381,51 @@ def main():
     qr_cmp["note"] = ("same filtered block; paper Table 3 (P:455-483) compares ChASE with HHQR "
                       "(ScaLAPACK, CPU) against CholeskyQR; here both run on the GPU")
 
-    # ---- end-to-end through the public API with host buffers (V in from pinned host, V out)
+    # ---- end-to-end through the public API with host buffers: every step's V is copied in from
+    # pinned host memory and its result copied back out.  Double-buffered like a production
+    # caller: step k+1's H2D and step k's D2H run on a copy stream under step k / k+1's compute.
     e2e = None
     if not args.no_e2e:
+        bufs = [V_t, torch.empty_like(V_t)]
+        cstream = torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(args.steps)]
+        ev_done = [torch.cuda.Event() for _ in range(args.steps)]
+        ev_out = torch.cuda.Event()
+
+        def run_e2e():
+            cstream.wait_stream(stream)
+            with torch.cuda.stream(cstream):
+                bufs[0].copy_(V0_host, non_blocking=True)
+                ev_in[0].record(cstream)
+            for k in range(args.steps):
+                vb = bufs[k % 2]
+                stream.wait_event(ev_in[k])
+                h.filter(A_local, vb.T, degrees, b.c, b.e, bounds)
+                h.cholqr(vb.T, est)
+                ev_done[k].record(stream)
+                with torch.cuda.stream(cstream):
+                    if k + 1 < args.steps:
+                        bufs[(k + 1) % 2].copy_(V0_host, non_blocking=True)
+                        ev_in[k + 1].record(cstream)
+                    cstream.wait_event(ev_done[k])
+                    out_host.copy_(vb, non_blocking=True)
+            ev_out.record(cstream)
+            stream.wait_event(ev_out)
+
         barrier()
         e0.record(stream)
-        for _ in range(args.steps):
-            V_t.copy_(V0_host, non_blocking=True)
-            step()
-            out_host.copy_(V_t, non_blocking=True)
+        run_e2e()
         e1.record(stream)
         barrier()
         e2e_ms = allmax(e0.elapsed_time(e1))
+        del bufs
         nbytes = V0_host.numel() * V0_host.element_size()
         e2e = {"value": F * args.steps / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": int(nbytes),
                "d2h_bytes_per_step": int(nbytes),
-               "note": "A_local resident (set once, as the paper distributes H once); V copied in and out every step"}
+               "note": "A_local resident (set once, as the paper distributes H once); V copied in from "
+                       "pinned host memory and the result out every step, double-buffered on a copy "
+                       "stream (step k+1 in and step k out overlap compute)"}
 
     # ---- CPU oracle baseline on a bounded sample of the same workload (rank 0, N=1)
     cpu = None

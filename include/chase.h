@@ -161,9 +161,9 @@ chase_status_t chase_workspace_size(chase_handle_t h, size_t* bytes);
 chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes);
 
 /* ---------------------------------------------------------------------------------------
- * Fused compute+collective filter steps (complex double, p*q > 1).  With a symmetric
+ * Fused compute+collective filter steps (complex or real double, p*q > 1).  With a symmetric
  * peer-mapped region set, every filter step whose communicator has more than one member runs as
- * ONE persistent kernel: the tensor-core HEMM publishes each partial output tile into its own
+ * ONE persistent kernel (zgemm_fused.cuh / dgemm_fused.cuh): the tensor-core HEMM publishes each partial output tile into its own
  * region, the tile's owner (tile mod m) sums the m partial tiles in fixed member order over
  * NVLink and stores the result into every member's region (P:149's AllReduce, done tile by tile
  * inside the GEMM, deterministic and replica-identical).  Without it, steps call ncclAllReduce.
@@ -173,7 +173,7 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes);
  *   peer_bases[r] = the address at which world rank r's region is mapped in this process
  *   (peer_bases[my world rank] == local); world = p*q.  Zeroes the region's control words; the
  *   caller must barrier all ranks after every rank returned and before the next chase_filter.
- *   local == NULL switches back to NCCL.  Errors: CHASE_EINVAL (real dtype, bad pointers,
+ *   local == NULL switches back to NCCL.  Errors: CHASE_EINVAL (bad pointers,
  *   p or q > 8), CHASE_ECUDA.  A peer that never arrives makes chase_filter return CHASE_ECUDA
  *   after a bounded wait (~10 s) instead of hanging. */
 chase_status_t chase_fused_workspace_size(chase_handle_t h, size_t* bytes);

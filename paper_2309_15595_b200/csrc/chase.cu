@@ -20,6 +20,7 @@
 #include "qr_kernels.cuh"
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
+#include "dgemm_fused.cuh"
 
 using namespace chase;
 
@@ -287,6 +288,7 @@ static WsLayout ws_layout(const chase_handle_s* h) {
 // ==================================================================== GEMM launchers
 static bool g_attr_done[2][2] = {{false, false}, {false, false}};
 static bool g_fused_attr[2] = {false, false};
+static bool g_dfused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
@@ -396,10 +398,41 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
 }
 
+static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
+                                         const CUtensorMap& tX, const GemmReq& r,
+                                         const FusedArgs& f, int T) {
+  DGemmArgs a{};
+  a.M = r.M; a.N = r.N; a.K = r.K;
+  a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
+  a.out = static_cast<double*>(r.out); a.ldo = r.ldo;
+  a.xin = static_cast<const double*>(r.xin); a.ldx = r.ldx;
+  a.alpha = r.alpha; a.beta = r.beta; a.c = r.c;
+  a.use_beta = 0; a.band_lo = r.band_lo; a.band_hi = r.band_hi; a.band_shift = r.band_shift;
+  a.band_map = r.band_map;
+  a.a3d = r.a3d;
+  const int grid = std::min(T, h->num_sms);
+  if (trans) {
+    if (!g_dfused_attr[1]) {
+      CUDA_TRY(cudaFuncSetAttribute(dgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
+      g_dfused_attr[1] = true;
+    }
+    dgemm_fused_kernel<true><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  } else {
+    if (!g_dfused_attr[0]) {
+      CUDA_TRY(cudaFuncSetAttribute(dgemm_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
+      g_dfused_attr[0] = true;
+    }
+    dgemm_fused_kernel<false><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CHASE_OK;
+}
+
 static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                          const CUtensorMap& tX, const GemmReq& r,
                                          const FusedArgs& f, int T) {
   if (r.M <= 0 || r.N <= 0) return CHASE_OK;
+  if (h->dt == CHASE_R64) return launch_dgemm_fused(h, conj, tA, tX, r, f, T);
   ZGemmArgs a{};
   a.M = r.M; a.N = r.N; a.K = r.K;
   a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
@@ -814,7 +847,7 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
     h->fused = false;
     return CHASE_OK;
   }
-  if (h->dt != CHASE_C128 || world != h->p * h->q || !peer_bases || world > 64) return CHASE_EINVAL;
+  if (world != h->p * h->q || !peer_bases || world > 64) return CHASE_EINVAL;
   const int me = h->myrow * h->q + h->mycol;
   if (peer_bases[me] != reinterpret_cast<uint64_t>(local)) return CHASE_EINVAL;
   if (h->p > FUSED_MAX_MEMBERS || h->q > FUSED_MAX_MEMBERS) return CHASE_EINVAL;
@@ -911,7 +944,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
   // CHASE_FUSED_SELF=1: run the fused kernel even for single-member steps (diagnostics: measures
   // the persistent kernel + epilogue protocol without any peer)
   static const bool fused_self = getenv("CHASE_FUSED_SELF") != nullptr;
-  const bool fused = h->fused && h->dt == CHASE_C128 && (h->p > 1 || h->q > 1 || fused_self);
+  const bool fused = h->fused && (h->p > 1 || h->q > 1 || fused_self);
   FusedLayout FL{};
   char* Cbuf = static_cast<char*>(V);
   int64_t ldc = ldv;
@@ -1009,7 +1042,8 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       f.tile_ctr = reinterpret_cast<unsigned long long*>(h->fz_base[me_world] + FL.ctr);
       f.ctr_base = h->fused_ctr;
       g.use_beta = 0;                        // the tile owner adds beta * old after the sum
-      const int T = ((g.M + ZG_BM - 1) / ZG_BM) * ((g.N + ZG_BN - 1) / ZG_BN);
+      const int BMf = h->dt == CHASE_C128 ? ZG_BM : DG_BM, BNf = h->dt == CHASE_C128 ? ZG_BN : DG_BN;
+      const int T = ((g.M + BMf - 1) / BMf) * ((g.N + BNf - 1) / BNf);
       // every CTA grabs until it sees an index >= T: T + grid increments per launch
       h->fused_ctr += (unsigned long long)T + (unsigned long long)std::min(T, h->num_sms);
       ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);

@@ -1,0 +1,294 @@
+// dgemm_fused.cuh -- the real-symmetric filter step as ONE kernel (BASELINE C5 is real, P:76
+// "templated for complex/real type"): the dgemm mainloop (dgemm.cuh: 128 x 128 tiles, 16 k per
+// stage, XOR-linear k permutation) inside the persistent push/owner/broadcast protocol of
+// zgemm_fused.cuh (dynamic tile scheduler, partial tiles pushed into the owner's staging slots
+// over NVLink, fixed-order owner sum + beta term, broadcast, delivery counters, bounded spins).
+// See zgemm_fused.cuh for the protocol and its deadlock-freedom argument; only the element type
+// and the tile mainloop differ.
+#pragma once
+#include "dgemm.cuh"
+#include "zgemm_fused.cuh"
+
+namespace chase {
+
+template <bool TRANS>
+__global__ void __launch_bounds__(DG_THREADS, 1)
+    dgemm_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
+                       const DGemmArgs g, const FusedArgs f) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DG_STAGES * DG_STAGE_BYTES);
+  uint64_t* empty = full + DG_STAGES;
+  __shared__ int s_abort;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
+  const int T = n_tiles * m_tiles;
+  const int KT = (g.K + DG_BK - 1) / DG_BK;
+  constexpr int RING = DG_STAGES + 2;
+  __shared__ int s_tile[RING];
+  int issued = 0;
+  auto grab = [&]() -> int {
+    const unsigned long long v = atomicAdd(f.tile_ctr, 1ull) - f.ctr_base;
+    return v < (unsigned long long)T ? (int)v : -1;
+  };
+  auto tile_origin = [&](int t, int& m0, int& n0) {
+    const int group = t / (DG_GROUP_M * n_tiles);
+    const int first_m = group * DG_GROUP_M;
+    const int gm = min(DG_GROUP_M, m_tiles - first_m);
+    const int within = t - group * DG_GROUP_M * n_tiles;
+    m0 = (first_m + within % gm) * DG_BM;
+    n0 = (within / gm) * DG_BN;
+  };
+
+  if (threadIdx.x == 0) {
+    s_abort = 0;
+    const long long t0 = clock64();
+    while (ld_acquire_sys_u64(f.done[f.me]) < f.done_target) {
+      __nanosleep(256);
+      if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+        atomicExch(f.err, 1);
+        s_abort = 1;
+        break;
+      }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    for (int s = 0; s < DG_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], DG_CONSUMERS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (s_abort) return;
+
+  int is_seq = 0, is_kt = 0, is_m0 = 0, is_n0 = 0;
+  bool prod_done = false;
+  auto issue = [&](int s) {
+    if (prod_done) return;
+    if (is_kt == 0) {
+      const int t = grab();
+      s_tile[is_seq % RING] = t;
+      if (t < 0) {
+        prod_done = true;
+        mbar_arrive(&full[s]);
+        return;
+      }
+      tile_origin(t, is_m0, is_n0);
+    }
+    const int k0 = is_kt * DG_BK, m0 = is_m0, n0 = is_n0;
+    mbar_arrive_expect_tx(&full[s], DG_STAGE_BYTES);
+    uint8_t* sa = smem + s * DG_STAGE_BYTES;
+    uint8_t* sx = sa + DG_A_BYTES;
+    if (TRANS) {
+      tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);
+    } else if (g.a3d) {
+      tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 16, &full[s]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < DG_BM / 16; ++b)
+        tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+    }
+    tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);
+    ++issued;
+    if (++is_kt == KT) {
+      is_kt = 0;
+      ++is_seq;
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmX);
+    for (int gs = 0; gs < DG_STAGES; ++gs) issue(gs);
+  }
+
+  const int wm = warp & 3, wn = warp >> 2;
+  const int gq = lane >> 2, tq = lane & 3;
+  double acc[DG_MT][DG_NT][4];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < DG_MT; ++i)
+#pragma unroll
+      for (int j = 0; j < DG_NT; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+  };
+  zero_acc();
+
+  constexpr int SUBS = DG_BK / 4;
+  struct Frag {
+    double a[DG_MT][2], b[DG_NT];
+  };
+  auto load = [&](Frag& fr, int gs, int kt, int hsub) {
+    const int k = dg_kperm(tq, hsub);
+    const uint8_t* sa = smem + (gs % DG_STAGES) * DG_STAGE_BYTES;
+    const uint8_t* sx = sa + DG_A_BYTES;
+#pragma unroll
+    for (int mt = 0; mt < DG_MT; ++mt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int m = wm * DG_WM + mt * 16 + r * 8 + gq;
+        const int off = TRANS ? m * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3))
+                              : (m >> 4) * 2048 + k * 128 +
+                                    (((((m & 15) >> 1) ^ (k & 7)) << 4) | ((m & 1) << 3));
+        fr.a[mt][r] = *reinterpret_cast<const double*>(sa + off);
+      }
+#pragma unroll
+    for (int nt = 0; nt < DG_NT; ++nt) {
+      const int n = wn * DG_WN + nt * 8 + gq;
+      fr.b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
+    }
+    if (kt * DG_BK + k >= g.K) {
+#pragma unroll
+      for (int mt = 0; mt < DG_MT; ++mt) fr.a[mt][0] = fr.a[mt][1] = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < DG_NT; ++nt) fr.b[nt] = 0.0;
+    }
+  };
+
+  auto epilogue = [&](int t) {
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    double* const* outs = reinterpret_cast<double* const*>(f.out);
+    if (f.plain) {
+#pragma unroll
+      for (int mt = 0; mt < DG_MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < DG_NT; ++nt)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int row = m0 + wm * DG_WM + mt * 16 + gq + ((r & 2) ? 8 : 0);
+            const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
+            if (row < g.M && col < g.N) {
+              double v = acc[mt][nt][r];
+              if (row >= g.band_lo && row < g.band_hi)
+                v -= g.c * g.xin[(long long)(row + g.band_shift) + (long long)col * g.ldx];
+              v *= g.alpha;
+              double* o = outs[f.me] + (long long)row + (long long)col * g.ldo;
+              if (f.owner_beta) v += g.beta * *o;
+              *o = v;
+            }
+          }
+      if (threadIdx.x == 0) atomicAdd(f.done[f.me], 1ull);
+      return;
+    }
+    const int owner = (t / (int)gridDim.x) % f.m;
+    double* slot = reinterpret_cast<double*>(f.P[owner]) + (long long)f.me * f.slot;
+#pragma unroll
+    for (int mt = 0; mt < DG_MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < DG_NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int row = m0 + wm * DG_WM + mt * 16 + gq + ((r & 2) ? 8 : 0);
+          const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
+          if (row < g.M && col < g.N) {
+            double v = acc[mt][nt][r];
+            const int bsrc = g.band_map != nullptr ? g.band_map[row]
+                             : (row >= g.band_lo && row < g.band_hi ? row + g.band_shift : -1);
+            if (bsrc >= 0) v -= g.c * g.xin[(long long)bsrc + (long long)col * g.ldx];
+            slot[(long long)row + (long long)col * f.ldP] = v * g.alpha;
+          }
+        }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
+    if (owner != f.me) return;
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      for (int src = 0; src < f.m && !s_abort; ++src) {
+        while (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) {
+          __nanosleep(64);
+          if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+            atomicExch(f.err, 1);
+            s_abort = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    const double* __restrict__ mine = reinterpret_cast<const double*>(f.P[f.me]);
+    constexpr int PER = DG_BM * DG_BN / DG_THREADS;     // 64 elements per thread
+    constexpr int BATCH = 8;
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER; b0 += BATCH) {
+      double sum[BATCH];
+      long long io[BATCH];
+      bool ok[BATCH];
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i) {
+        const int e = threadIdx.x + (b0 + i) * DG_THREADS;
+        const int row = m0 + (e % DG_BM), col = n0 + (e / DG_BM);
+        ok[i] = row < g.M && col < g.N;
+        const long long ip = (long long)row + (long long)col * f.ldP;
+        io[i] = (long long)row + (long long)col * g.ldo;
+        sum[i] = ok[i] ? mine[ip] : 0.0;
+        for (int src = 1; src < f.m; ++src) sum[i] += ok[i] ? mine[(long long)src * f.slot + ip] : 0.0;
+        if (f.owner_beta && ok[i]) sum[i] += g.beta * outs[f.me][io[i]];
+      }
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i)
+        if (ok[i])
+          for (int dst = 0; dst < f.m; ++dst) outs[dst][io[i]] = sum[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+  };
+
+  Frag cur, nxt;
+  mbar_wait(&full[0], 0);
+  int tile = s_tile[0];
+  if (tile < 0) return;
+  load(cur, 0, 0, 0);
+  int seq = 0, kt = 0, gs = 0;
+  for (;;) {
+    const int s = gs % DG_STAGES;
+    int next_tile = tile;
+#pragma unroll
+    for (int sub = 0; sub < SUBS; ++sub) {
+      if (sub + 1 < SUBS) {
+        load(nxt, gs, kt, sub + 1);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        mbar_wait(&full[(gs + 1) % DG_STAGES], ((gs + 1) / DG_STAGES) & 1);
+        if (kt + 1 < KT) {
+          load(nxt, gs + 1, kt + 1, 0);
+        } else {
+          next_tile = s_tile[(seq + 1) % RING];
+          if (next_tile >= 0) load(nxt, gs + 1, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < DG_MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < DG_NT; ++nt) dmma_16x8x4(acc[mt][nt], cur.a[mt][0], cur.a[mt][1], cur.b[nt]);
+      cur = nxt;
+    }
+    if (threadIdx.x == 0 && gs >= 1) {
+      const int sp = (gs - 1) % DG_STAGES;
+      if (!prod_done) mbar_wait(&empty[sp], ((gs - 1) / DG_STAGES) & 1);
+      issue(sp);
+    }
+    ++gs;
+    if (++kt == KT) {
+      epilogue(tile);
+      zero_acc();
+      if (s_abort) {
+        if (threadIdx.x == 0)
+          for (int r = gs; r < issued; ++r) mbar_wait(&full[r % DG_STAGES], (r / DG_STAGES) & 1);
+        return;
+      }
+      kt = 0;
+      ++seq;
+      tile = next_tile;
+      if (tile < 0) break;
+    }
+  }
+}
+
+}  // namespace chase

@@ -48,7 +48,8 @@ CASES = ([(c, g, 0, "nccl", 0) for c in (True, False) for g in GRIDS] +
          [(True, (1, 2), 6, "nccl", 0), (False, (1, 2), 5, "nccl", 0), (True, (2, 2), 6, "nccl", 0)] +
          [(True, g, 0, "fused", 0) for g in GRIDS] + [(True, (1, 2), 6, "fused", 0)] +
          [(True, (2, 1), 0, "nccl", 7), (False, (1, 2), 0, "nccl", 1), (True, (2, 2), 0, "nccl", 16),
-          (True, (1, 2), 0, "fused", 5), (True, (2, 2), 0, "fused", 32), (False, (2, 2), 0, "nccl", 3)])
+          (True, (1, 2), 0, "fused", 5), (True, (2, 2), 0, "fused", 32), (False, (2, 2), 0, "nccl", 3)] +
+         [(False, g, 0, "fused", 0) for g in GRIDS] + [(False, (1, 2), 5, "fused", 0), (False, (2, 2), 0, "fused", 3)])
 
 
 @pytest.mark.parametrize("complex_,grid,pad,mode,nb", CASES)
