@@ -1040,12 +1040,12 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       static const bool plain = getenv("CHASE_FUSED_PLAIN") != nullptr;
       f.plain = (m == 1 && plain) ? 1 : 0;
       f.tile_ctr = reinterpret_cast<unsigned long long*>(h->fz_base[me_world] + FL.ctr);
-      f.ctr_base = h->fused_ctr;
+      f.ctr_base = 0;                        // local counter, reset per launch (stream-ordered):
+      CUDA_TRY(cudaMemsetAsync(f.tile_ctr, 0, sizeof(unsigned long long), h->stream));   // CTAs
+      //   grab ahead, so the number of grabs per launch is not fixed
       g.use_beta = 0;                        // the tile owner adds beta * old after the sum
       const int BMf = h->dt == CHASE_C128 ? ZG_BM : DG_BM, BNf = h->dt == CHASE_C128 ? ZG_BN : DG_BN;
       const int T = ((g.M + BMf - 1) / BMf) * ((g.N + BNf - 1) / BNf);
-      // every CTA grabs until it sees an index >= T: T + grid increments per launch
-      h->fused_ctr += (unsigned long long)T + (unsigned long long)std::min(T, h->num_sms);
       ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
       STATUS_TRY(launch_zgemm_fused(h, g.conj, *g.tA, *g.tX, g, f, T));
       h->fused_delivered += (unsigned long long)T;

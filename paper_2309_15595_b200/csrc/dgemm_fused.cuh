@@ -25,9 +25,8 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
   const int T = n_tiles * m_tiles;
   const int KT = (g.K + DG_BK - 1) / DG_BK;
-  constexpr int RING = DG_STAGES + 2;
+  constexpr int RING = DG_STAGES + 4;                  // see zgemm_fused.cuh (grab 2 ahead)
   __shared__ int s_tile[RING];
-  int issued = 0;
   auto grab = [&]() -> int {
     const unsigned long long v = atomicAdd(f.tile_ctr, 1ull) - f.ctr_base;
     return v < (unsigned long long)T ? (int)v : -1;
@@ -62,21 +61,19 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   __syncthreads();
   if (s_abort) return;
 
-  int is_seq = 0, is_kt = 0, is_m0 = 0, is_n0 = 0;
-  bool prod_done = false;
-  auto issue = [&](int s) {
-    if (prod_done) return;
-    if (is_kt == 0) {
-      const int t = grab();
-      s_tile[is_seq % RING] = t;
-      if (t < 0) {
-        prod_done = true;
-        mbar_arrive(&full[s]);
-        return;
-      }
-      tile_origin(t, is_m0, is_n0);
+  auto issue = [&](int q, int s) {
+    if ((q + 2) % KT == 0) {
+      const int sq = (q + 2) / KT;
+      s_tile[sq % RING] = grab();
     }
-    const int k0 = is_kt * DG_BK, m0 = is_m0, n0 = is_n0;
+    const int t = s_tile[(q / KT) % RING];
+    if (t < 0) {
+      mbar_arrive(&full[s]);
+      return;
+    }
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    const int k0 = (q % KT) * DG_BK;
     mbar_arrive_expect_tx(&full[s], DG_STAGE_BYTES);
     uint8_t* sa = smem + s * DG_STAGE_BYTES;
     uint8_t* sx = sa + DG_A_BYTES;
@@ -90,16 +87,12 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
     }
     tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);
-    ++issued;
-    if (++is_kt == KT) {
-      is_kt = 0;
-      ++is_seq;
-    }
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmX);
-    for (int gs = 0; gs < DG_STAGES; ++gs) issue(gs);
+    for (int sq = 0; sq * KT < 2; ++sq) s_tile[sq % RING] = grab();
+    for (int gs = 0; gs < DG_STAGES; ++gs) issue(gs, gs);
   }
 
   const int wm = warp & 3, wn = warp >> 2;
@@ -269,10 +262,10 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         for (int nt = 0; nt < DG_NT; ++nt) dmma_16x8x4(acc[mt][nt], cur.a[mt][0], cur.a[mt][1], cur.b[nt]);
       cur = nxt;
     }
-    if (threadIdx.x == 0 && gs >= 1) {
+    if (lane == 0 && warp == (gs & (DG_CONSUMERS - 1)) && gs >= 1) {
       const int sp = (gs - 1) % DG_STAGES;
-      if (!prod_done) mbar_wait(&empty[sp], ((gs - 1) / DG_STAGES) & 1);
-      issue(sp);
+      mbar_wait(&empty[sp], ((gs - 1) / DG_STAGES) & 1);
+      issue(gs - 1 + DG_STAGES, sp);
     }
     ++gs;
     if (++kt == KT) {
@@ -280,7 +273,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       zero_acc();
       if (s_abort) {
         if (threadIdx.x == 0)
-          for (int r = gs; r < issued; ++r) mbar_wait(&full[r % DG_STAGES], (r / DG_STAGES) & 1);
+          for (int r = gs; r < gs + DG_STAGES - 1; ++r) mbar_wait(&full[r % DG_STAGES], (r / DG_STAGES) & 1);
         return;
       }
       kt = 0;

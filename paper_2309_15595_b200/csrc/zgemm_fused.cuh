@@ -15,6 +15,8 @@
 // until its delivery counter covers the whole previous step.  The reduction traffic of tile t
 // overlaps the math of the tiles that follow it -- no separate collective launch.
 //
+// The k-tile loads are refilled by the MMA warps in rotation (no producer warp); the tile id of
+// each sequence position is grabbed from the global counter two issue indices ahead.
 // Deadlock freedom: all CTAs are co-resident (grid <= #SMs, 1 CTA/SM) and every member walks the
 // same tile sequence per CTA; a partial is always published before its producer waits on
 // anything, so the wait at sequence position i only depends on positions <= i of the peers.
@@ -74,11 +76,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   const int T = n_tiles * m_tiles;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
-  // dynamic tile scheduler: the producer grabs the next tile from a global counter and passes it
-  // to the MMA warps through a small smem ring (tile -1 = no more tiles)
-  constexpr int RING = ZG_STAGES + 2;
+  // dynamic tile scheduler: tiles come from a global counter into a small smem ring (tile -1 =
+  // no more tiles).  k-tile issue index q maps to (seq, kt) = (q / KT, q % KT); the refill duty
+  // rotates over the 8 MMA warps (as in zgemm.cuh), and a refill only sees the smem writes of
+  // refills >= 2 iterations older (mbarrier ordering), so the tile of sequence position s is
+  // grabbed two issue indices ahead, by the refill that issues q = s KT - 2.
+  constexpr int RING = ZG_STAGES + 4;
   __shared__ int s_tile[RING];
-  int issued = 0;                                      // k-tiles with TMA in flight (thread 0)
   auto grab = [&]() -> int {
     const unsigned long long v = atomicAdd(f.tile_ctr, 1ull) - f.ctr_base;
     return v < (unsigned long long)T ? (int)v : -1;
@@ -114,24 +118,20 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   __syncthreads();
   if (s_abort) return;
 
-  // k-tile stream: issue() is called by thread 0 for gs = 0, 1, 2, ... in order; (tile, kt, m0,
-  // n0) of the next load advance incrementally.  When the scheduler runs dry the stage gets a
-  // plain arrive (no bytes) and its ring entry says -1.
-  int is_seq = 0, is_kt = 0, is_m0 = 0, is_n0 = 0;
-  bool prod_done = false;
-  auto issue = [&](int s) {
-    if (prod_done) return;
-    if (is_kt == 0) {
-      const int t = grab();
-      s_tile[is_seq % RING] = t;
-      if (t < 0) {
-        prod_done = true;
-        mbar_arrive(&full[s]);
-        return;
-      }
-      tile_origin(t, is_m0, is_n0);
+  // issue k-tile q into stage s (one lane); a stage past the last tile gets a plain arrive
+  auto issue = [&](int q, int s) {
+    if ((q + 2) % KT == 0) {
+      const int sq = (q + 2) / KT;
+      s_tile[sq % RING] = grab();
     }
-    const int kt = is_kt, m0 = is_m0, n0 = is_n0;
+    const int t = s_tile[(q / KT) % RING];
+    if (t < 0) {
+      mbar_arrive(&full[s]);
+      return;
+    }
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    const int kt = q % KT;
     mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
     uint8_t* sa = smem + s * ZG_STAGE_BYTES;
     uint8_t* sx = sa + ZG_A_BYTES;
@@ -150,16 +150,12 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       }
       tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
-    ++issued;
-    if (++is_kt == KT) {
-      is_kt = 0;
-      ++is_seq;
-    }
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmX);
-    for (int gs = 0; gs < ZG_STAGES; ++gs) issue(gs);
+    for (int sq = 0; sq * KT < 2; ++sq) s_tile[sq % RING] = grab();   // tiles with q_grab < 0
+    for (int gs = 0; gs < ZG_STAGES; ++gs) issue(gs, gs);
   }
 
   const int wm = warp & 3, wn = warp >> 2;
@@ -366,18 +362,21 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       mma(cur);
       cur = nxt;
     }
-    if (threadIdx.x == 0 && gs >= 1) {
+    // refill the stage released one iteration ago; the duty rotates over the warps
+    if (lane == 0 && warp == (gs & (ZG_CONSUMERS - 1)) && gs >= 1) {
       const int sp = (gs - 1) % ZG_STAGES;
-      if (!prod_done) mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
-      issue(sp);
+      mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
+      issue(gs - 1 + ZG_STAGES, sp);
     }
     ++gs;
     if (++kt == KT) {
       epilogue(tile);
       zero_acc();
       if (s_abort) {              // a peer never arrived: give up (the host reports CHASE_ECUDA)
-        if (threadIdx.x == 0)     // let the loads already in flight land before the CTA exits
-          for (int r = gs; r < issued; ++r) mbar_wait(&full[r % ZG_STAGES], (r / ZG_STAGES) & 1);
+        // every refill up to iteration gs - 1 is done (the epilogue synchronised the CTA): let the
+        // loads of issue indices gs .. gs + STAGES - 2 land before the CTA exits
+        if (threadIdx.x == 0)
+          for (int r = gs; r < gs + ZG_STAGES - 1; ++r) mbar_wait(&full[r % ZG_STAGES], (r / ZG_STAGES) & 1);
         return;
       }
       kt = 0;
