@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libchase.so")
 SOURCES = ["chase.cu"]
-HEADERS = ["common.cuh", "zgemm.cuh", "dgemm.cuh", "qr_kernels.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".inc")))   # every included file
 
 
 def nccl_dirs():

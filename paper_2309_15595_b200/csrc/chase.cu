@@ -530,7 +530,7 @@ static chase_status_t allreduce_cols(chase_handle_s* h, void* buf, int64_t rows,
 //   Cw  C-layout working block  pad(ceil(N/p)) x n_max      (filter even-step outputs)
 //   Bw  B-layout working block  pad(ceil(N/q)) x n_max      (filter odd-step outputs)
 //   P   partial tiles           pad(max rows)  x n_max
-//   flags [tile * m + src] u32  (tiles of the largest step) x max(p, q)
+//   flags [tile * m + src] u32  (tiles of the largest step) x max(p, q), one array per parity
 //   done  u64 delivery counter, err i32
 struct FusedLayout {
   int64_t ldc, ldb, ldpo, ldpe;
@@ -570,7 +570,7 @@ static FusedLayout fused_layout(const chase_handle_s* h) {
   L.pe = off;
   off += align256((size_t)h->q * L.ldpe * h->n_max * 16);
   L.flags = off;
-  off += align256((size_t)L.tiles_max * std::max(h->p, h->q) * sizeof(unsigned));
+  off += align256((size_t)2 * L.tiles_max * std::max(h->p, h->q) * sizeof(unsigned));
   L.done = off;
   off += 256;
   L.err = off;
@@ -1028,7 +1028,10 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
         f.P[i] = reinterpret_cast<double2*>(base + (odd ? FL.po : FL.pe));
         f.out[i] = reinterpret_cast<double2*>(base + (odd ? FL.bw + (size_t)r.off * FL.ldb * es
                                                           : FL.cw + (size_t)r.off * FL.ldc * es));
-        f.flags[i] = reinterpret_cast<unsigned*>(base + FL.flags);
+        // one flag array per step parity: the two communicators of a rank progress independently,
+        // so a peer already in step s+1 must not overwrite flags this rank still reads for step s
+        f.flags[i] = reinterpret_cast<unsigned*>(base + FL.flags) +
+                     (odd ? 0 : (size_t)FL.tiles_max * std::max(h->p, h->q));
         f.done[i] = reinterpret_cast<unsigned long long*>(base + FL.done);
       }
       f.ldP = odd ? FL.ldpo : FL.ldpe;

@@ -40,6 +40,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Debug variant (CHASE_MBAR_DEBUG builds): bounded wait that reports who is stuck and traps.
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, int it) {
+#ifdef CHASE_MBAR_DEBUG
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 8000000000LL) {
+      printf("[mbar] stuck: block %d thread %d tag %d it %d parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, tag, it, parity);
+      asm volatile("trap;");
+    }
+  }
+#else
+  (void)tag;
+  (void)it;
+  mbar_wait(bar, parity);
+#endif
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

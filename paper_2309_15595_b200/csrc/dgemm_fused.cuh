@@ -20,6 +20,8 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DG_STAGES * DG_STAGE_BYTES);
   uint64_t* empty = full + DG_STAGES;
   __shared__ int s_abort;
+  __shared__ int s_q[FUSED_QCAP];
+  __shared__ int s_qh, s_qt, s_cmd;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
@@ -42,10 +44,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
 
   if (threadIdx.x == 0) {
     s_abort = 0;
+    s_qh = s_qt = 0;
     const long long t0 = clock64();
     while (ld_acquire_sys_u64(f.done[f.me]) < f.done_target) {
       __nanosleep(256);
       if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+        printf("[chase fused] member %d CTA %d: previous step not delivered (%llu < %llu)\n", f.me,
+               (int)blockIdx.x, ld_acquire_sys_u64(f.done[f.me]), f.done_target);
         atomicExch(f.err, 1);
         s_abort = 1;
         break;
@@ -139,6 +144,87 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     }
   };
 
+  // owner side: fixed-order sum of the m partial tiles of t (local slots), + beta V_{s-2},
+  // broadcast into every member's output, delivery counters bumped
+  auto reduce = [&](int t) {
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    double* const* outs = reinterpret_cast<double* const*>(f.out);
+    const double* __restrict__ mine = reinterpret_cast<const double*>(f.P[f.me]);
+    constexpr int PER = DG_BM * DG_BN / DG_THREADS;     // 64 elements per thread
+    constexpr int BATCH = 8;
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER; b0 += BATCH) {
+      double sum[BATCH];
+      long long io[BATCH];
+      bool ok[BATCH];
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i) {
+        const int e = threadIdx.x + (b0 + i) * DG_THREADS;
+        const int row = m0 + (e % DG_BM), col = n0 + (e / DG_BM);
+        ok[i] = row < g.M && col < g.N;
+        const long long ip = (long long)row + (long long)col * f.ldP;
+        io[i] = (long long)row + (long long)col * g.ldo;
+        sum[i] = ok[i] ? mine[ip] : 0.0;
+        for (int src = 1; src < f.m; ++src) sum[i] += ok[i] ? mine[(long long)src * f.slot + ip] : 0.0;
+        if (f.owner_beta && ok[i]) sum[i] += g.beta * outs[f.me][io[i]];
+      }
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i)
+        if (ok[i])
+          for (int dst = 0; dst < f.m; ++dst) outs[dst][io[i]] = sum[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+  };
+
+  // Owned tiles wait in a small queue and are reduced as soon as all m partials are in, checked
+  // (without blocking) after every tile; the CTA blocks only when the queue is full and, at the
+  // end, until its queue is drained.  A straggling peer therefore never stalls the tensor pipe of
+  // an owner that still has tiles to compute.
+  auto flags_ready = [&](int t) -> bool {      // thread 0
+    for (int src = 0; src < f.m; ++src)
+      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) return false;
+    return true;
+  };
+  auto drain = [&](bool final_) {
+    for (;;) {
+      if (threadIdx.x == 0) {
+        int cmd = -1;
+        if (s_qh < s_qt) {
+          const int t = s_q[s_qh % FUSED_QCAP];
+          bool ok = flags_ready(t);
+          if (!ok && (final_ || s_qt - s_qh >= FUSED_QCAP)) {
+            const long long t0 = clock64();
+            while (!(ok = flags_ready(t))) {
+              __nanosleep(64);
+              if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+                printf("[chase fused] member %d CTA %d: tile %d partials missing (m %d, ep %u, flags %u %u, final %d, q %d..%d)\n",
+                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)t * f.m],
+                       f.flags[f.me][(long long)t * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
+                atomicExch(f.err, 1);
+                s_abort = 1;
+                break;
+              }
+            }
+          }
+          if (ok) {
+            cmd = t;
+            ++s_qh;
+          }
+        }
+        s_cmd = cmd;
+      }
+      __syncthreads();
+      const int t = s_cmd;
+      __syncthreads();                         // s_cmd read by all before thread 0 rewrites it
+      if (t < 0 || s_abort) return;
+      reduce(t);
+    }
+  };
+
   auto epilogue = [&](int t) {
     int m0, n0;
     tile_origin(t, m0, n0);
@@ -186,54 +272,15 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
-    if (owner != f.me) return;
-    if (threadIdx.x == 0) {
-      const long long t0 = clock64();
-      for (int src = 0; src < f.m && !s_abort; ++src) {
-        while (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) {
-          __nanosleep(64);
-          if (clock64() - t0 > FUSED_SPIN_CYCLES) {
-            atomicExch(f.err, 1);
-            s_abort = 1;
-            break;
-          }
-        }
-      }
+    if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
+      s_q[s_qt % FUSED_QCAP] = t;
+      ++s_qt;
     }
-    __syncthreads();
-    if (s_abort) return;
-    const double* __restrict__ mine = reinterpret_cast<const double*>(f.P[f.me]);
-    constexpr int PER = DG_BM * DG_BN / DG_THREADS;     // 64 elements per thread
-    constexpr int BATCH = 8;
-#pragma unroll 1
-    for (int b0 = 0; b0 < PER; b0 += BATCH) {
-      double sum[BATCH];
-      long long io[BATCH];
-      bool ok[BATCH];
-#pragma unroll
-      for (int i = 0; i < BATCH; ++i) {
-        const int e = threadIdx.x + (b0 + i) * DG_THREADS;
-        const int row = m0 + (e % DG_BM), col = n0 + (e / DG_BM);
-        ok[i] = row < g.M && col < g.N;
-        const long long ip = (long long)row + (long long)col * f.ldP;
-        io[i] = (long long)row + (long long)col * g.ldo;
-        sum[i] = ok[i] ? mine[ip] : 0.0;
-        for (int src = 1; src < f.m; ++src) sum[i] += ok[i] ? mine[(long long)src * f.slot + ip] : 0.0;
-        if (f.owner_beta && ok[i]) sum[i] += g.beta * outs[f.me][io[i]];
-      }
-#pragma unroll
-      for (int i = 0; i < BATCH; ++i)
-        if (ok[i])
-          for (int dst = 0; dst < f.m; ++dst) outs[dst][io[i]] = sum[i];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+    drain(false);
   };
 
   Frag cur, nxt;
-  mbar_wait(&full[0], 0);
+  mbar_wait_dbg(&full[0], 0, 1, 0);
   int tile = s_tile[0];
   if (tile < 0) return;
   load(cur, 0, 0, 0);
@@ -248,7 +295,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        mbar_wait(&full[(gs + 1) % DG_STAGES], ((gs + 1) / DG_STAGES) & 1);
+        mbar_wait_dbg(&full[(gs + 1) % DG_STAGES], ((gs + 1) / DG_STAGES) & 1, 2, gs);
         if (kt + 1 < KT) {
           load(nxt, gs + 1, kt + 1, 0);
         } else {
@@ -264,7 +311,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     }
     if (lane == 0 && warp == (gs & (DG_CONSUMERS - 1)) && gs >= 1) {
       const int sp = (gs - 1) % DG_STAGES;
-      mbar_wait(&empty[sp], ((gs - 1) / DG_STAGES) & 1);
+      mbar_wait_dbg(&empty[sp], ((gs - 1) / DG_STAGES) & 1, 3, gs);
       issue(gs - 1 + DG_STAGES, sp);
     }
     ++gs;
@@ -282,6 +329,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       if (tile < 0) break;
     }
   }
+  drain(true);                                 // the owned tiles still waiting
 }
 
 }  // namespace chase

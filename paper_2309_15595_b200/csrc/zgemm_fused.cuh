@@ -28,6 +28,7 @@
 namespace chase {
 
 constexpr int FUSED_MAX_MEMBERS = 8;
+constexpr int FUSED_QCAP = 8;        // owned tiles awaiting their peers' partials, per CTA
 
 struct FusedArgs {
   int m;                                     // communicator members (2..8)
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
   uint64_t* empty = full + ZG_STAGES;
   __shared__ int s_abort;
+  __shared__ int s_q[FUSED_QCAP];
+  __shared__ int s_qh, s_qt, s_cmd;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
@@ -98,11 +101,14 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   if (threadIdx.x == 0) {
     s_abort = 0;
+    s_qh = s_qt = 0;
     // inputs of this step are complete once every owner of the previous step has delivered
     const long long t0 = clock64();
     while (ld_acquire_sys_u64(f.done[f.me]) < f.done_target) {
       __nanosleep(256);
       if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+        printf("[chase fused] member %d CTA %d: previous step not delivered (%llu < %llu)\n", f.me,
+               (int)blockIdx.x, ld_acquire_sys_u64(f.done[f.me]), f.done_target);
         atomicExch(f.err, 1);
         s_abort = 1;
         break;
@@ -219,6 +225,96 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       }
   };
 
+  // owner side: fixed-order sum of the m partial tiles of t (local slots), + beta V_{s-2},
+  // broadcast into every member's output, delivery counters bumped
+  auto reduce = [&](int t) {
+    int m0, n0;
+    tile_origin(t, m0, n0);
+    // coalesced pass over the tile (column-major 128 x 64), partials read from local slots;
+    // 8 elements per thread per batch so the loads of a batch are all in flight together
+    const double2* __restrict__ mine = f.P[f.me];
+    constexpr int PER = ZG_BM * ZG_BN / ZG_THREADS;     // 32 elements per thread
+    constexpr int BATCH = 8;
+#pragma unroll 1
+    for (int b0 = 0; b0 < PER; b0 += BATCH) {
+      double2 sum[BATCH];
+      long long io[BATCH];
+      bool ok[BATCH];
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i) {
+        const int e = threadIdx.x + (b0 + i) * ZG_THREADS;
+        const int row = m0 + (e % ZG_BM), col = n0 + (e / ZG_BM);
+        ok[i] = row < g.M && col < g.N;
+        const long long ip = (long long)row + (long long)col * f.ldP;
+        io[i] = (long long)row + (long long)col * g.ldo;
+        sum[i] = ok[i] ? mine[ip] : make_double2(0.0, 0.0);
+        for (int src = 1; src < f.m; ++src) {
+          const double2 v = ok[i] ? mine[(long long)src * f.slot + ip] : make_double2(0.0, 0.0);
+          sum[i].x += v.x;
+          sum[i].y += v.y;
+        }
+        if (f.owner_beta && ok[i]) {
+          const double2 old = f.out[f.me][io[i]];
+          sum[i].x += g.beta * old.x;
+          sum[i].y += g.beta * old.y;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < BATCH; ++i)
+        if (ok[i])
+          for (int dst = 0; dst < f.m; ++dst) f.out[dst][io[i]] = sum[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+  };
+
+  // Owned tiles wait in a small queue and are reduced as soon as all m partials are in, checked
+  // (without blocking) after every tile; the CTA blocks only when the queue is full and, at the
+  // end, until its queue is drained.  A straggling peer therefore never stalls the tensor pipe of
+  // an owner that still has tiles to compute.
+  auto flags_ready = [&](int t) -> bool {      // thread 0
+    for (int src = 0; src < f.m; ++src)
+      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) return false;
+    return true;
+  };
+  auto drain = [&](bool final_) {
+    for (;;) {
+      if (threadIdx.x == 0) {
+        int cmd = -1;
+        if (s_qh < s_qt) {
+          const int t = s_q[s_qh % FUSED_QCAP];
+          bool ok = flags_ready(t);
+          if (!ok && (final_ || s_qt - s_qh >= FUSED_QCAP)) {
+            const long long t0 = clock64();
+            while (!(ok = flags_ready(t))) {
+              __nanosleep(64);
+              if (clock64() - t0 > FUSED_SPIN_CYCLES) {
+                printf("[chase fused] member %d CTA %d: tile %d partials missing (m %d, ep %u, flags %u %u, final %d, q %d..%d)\n",
+                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)t * f.m],
+                       f.flags[f.me][(long long)t * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
+                atomicExch(f.err, 1);
+                s_abort = 1;
+                break;
+              }
+            }
+          }
+          if (ok) {
+            cmd = t;
+            ++s_qh;
+          }
+        }
+        s_cmd = cmd;
+      }
+      __syncthreads();
+      const int t = s_cmd;
+      __syncthreads();                         // s_cmd read by all before thread 0 rewrites it
+      if (t < 0 || s_abort) return;
+      reduce(t);
+    }
+  };
+
   // epilogue of tile t: publish the partial, and reduce + broadcast it if this member owns t
   auto epilogue = [&](int t) {
     int m0, n0;
@@ -279,64 +375,15 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
-    if (owner != f.me) return;
-    if (threadIdx.x == 0) {
-      const long long t0 = clock64();
-      for (int src = 0; src < f.m && !s_abort; ++src) {
-        while (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) {
-          __nanosleep(64);
-          if (clock64() - t0 > FUSED_SPIN_CYCLES) {
-            atomicExch(f.err, 1);
-            s_abort = 1;
-            break;
-          }
-        }
-      }
+    if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
+      s_q[s_qt % FUSED_QCAP] = t;
+      ++s_qt;
     }
-    __syncthreads();
-    if (s_abort) return;
-    // coalesced pass over the tile (column-major 128 x 64), partials read from local slots;
-    // 8 elements per thread per batch so the loads of a batch are all in flight together
-    const double2* __restrict__ mine = f.P[f.me];
-    constexpr int PER = ZG_BM * ZG_BN / ZG_THREADS;     // 32 elements per thread
-    constexpr int BATCH = 8;
-#pragma unroll 1
-    for (int b0 = 0; b0 < PER; b0 += BATCH) {
-      double2 sum[BATCH];
-      long long io[BATCH];
-      bool ok[BATCH];
-#pragma unroll
-      for (int i = 0; i < BATCH; ++i) {
-        const int e = threadIdx.x + (b0 + i) * ZG_THREADS;
-        const int row = m0 + (e % ZG_BM), col = n0 + (e / ZG_BM);
-        ok[i] = row < g.M && col < g.N;
-        const long long ip = (long long)row + (long long)col * f.ldP;
-        io[i] = (long long)row + (long long)col * g.ldo;
-        sum[i] = ok[i] ? mine[ip] : make_double2(0.0, 0.0);
-        for (int src = 1; src < f.m; ++src) {
-          const double2 v = ok[i] ? mine[(long long)src * f.slot + ip] : make_double2(0.0, 0.0);
-          sum[i].x += v.x;
-          sum[i].y += v.y;
-        }
-        if (f.owner_beta && ok[i]) {
-          const double2 old = f.out[f.me][io[i]];
-          sum[i].x += g.beta * old.x;
-          sum[i].y += g.beta * old.y;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < BATCH; ++i)
-        if (ok[i])
-          for (int dst = 0; dst < f.m; ++dst) f.out[dst][io[i]] = sum[i];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+    drain(false);
   };
 
   Frag cur, nxt;
-  mbar_wait(&full[0], 0);
+  mbar_wait_dbg(&full[0], 0, 1, 0);
   int tile = s_tile[0];
   if (tile < 0) return;
   load(cur, 0, 0, 0);
@@ -351,7 +398,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        mbar_wait(&full[(gs + 1) % ZG_STAGES], ((gs + 1) / ZG_STAGES) & 1);
+        mbar_wait_dbg(&full[(gs + 1) % ZG_STAGES], ((gs + 1) / ZG_STAGES) & 1, 2, gs);
         if (kt + 1 < KT) {
           load(nxt, gs + 1, kt + 1, 0);
         } else {
@@ -365,7 +412,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     // refill the stage released one iteration ago; the duty rotates over the warps
     if (lane == 0 && warp == (gs & (ZG_CONSUMERS - 1)) && gs >= 1) {
       const int sp = (gs - 1) % ZG_STAGES;
-      mbar_wait(&empty[sp], ((gs - 1) / ZG_STAGES) & 1);
+      mbar_wait_dbg(&empty[sp], ((gs - 1) / ZG_STAGES) & 1, 3, gs);
       issue(gs - 1 + ZG_STAGES, sp);
     }
     ++gs;
@@ -385,6 +432,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       if (tile < 0) break;
     }
   }
+  drain(true);                                 // the owned tiles still waiting
 }
 
 // Waits (one thread) until *done >= target: the last step's tiles are all delivered before the
