@@ -286,7 +286,6 @@ static WsLayout ws_layout(const chase_handle_s* h) {
 
 
 // ==================================================================== GEMM launchers
-static bool g_attr_done[2][2] = {{false, false}, {false, false}};
 static bool g_fused_attr[2] = {false, false};
 static bool g_dfused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
@@ -294,24 +293,20 @@ static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B swi
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM) * std::max(1, a.k_split));
-  if (conj) {
-    if (!g_attr_done[1][0]) {
-      CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    ZG_SMEM_BYTES));
-      g_attr_done[1][0] = true;
+  const bool split = a.k_split > 1;
+  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM) * (split ? a.k_split : 1));
+  static bool attr[2][2] = {{false, false}, {false, false}};
+  auto go = [&](auto kern, bool& done) -> chase_status_t {
+    if (!done) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
+      done = true;
     }
-    zgemm_kernel<true><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
-  } else {
-    if (!g_attr_done[0][0]) {
-      CUDA_TRY(cudaFuncSetAttribute(zgemm_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
-      g_attr_done[0][0] = true;
-    }
-    zgemm_kernel<false><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
-  }
-  CUDA_TRY(cudaGetLastError());
-  return CHASE_OK;
+    kern<<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+    CUDA_TRY(cudaGetLastError());
+    return CHASE_OK;
+  };
+  if (conj) return split ? go(zgemm_kernel<true, true>, attr[1][1]) : go(zgemm_kernel<true>, attr[1][0]);
+  return split ? go(zgemm_kernel<false, true>, attr[0][1]) : go(zgemm_kernel<false>, attr[0][0]);
 }
 
 static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
@@ -321,24 +316,20 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
-  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM) * std::max(1, a.k_split));
-  if (trans) {
-    if (!g_attr_done[1][1]) {
-      CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    DG_SMEM_BYTES));
-      g_attr_done[1][1] = true;
+  const bool split = a.k_split > 1;
+  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM) * (split ? a.k_split : 1));
+  static bool attr[2][2] = {{false, false}, {false, false}};
+  auto go = [&](auto kern, bool& done) -> chase_status_t {
+    if (!done) {
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
+      done = true;
     }
-    dgemm_kernel<true><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
-  } else {
-    if (!g_attr_done[0][1]) {
-      CUDA_TRY(cudaFuncSetAttribute(dgemm_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
-      g_attr_done[0][1] = true;
-    }
-    dgemm_kernel<false><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
-  }
-  CUDA_TRY(cudaGetLastError());
-  return CHASE_OK;
+    kern<<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+    CUDA_TRY(cudaGetLastError());
+    return CHASE_OK;
+  };
+  if (trans) return split ? go(dgemm_kernel<true, true>, attr[1][1]) : go(dgemm_kernel<true>, attr[1][0]);
+  return split ? go(dgemm_kernel<false, true>, attr[0][1]) : go(dgemm_kernel<false>, attr[0][0]);
 }
 
 // One generic GEMM request, dispatched on the handle's dtype.  Pointers are element pointers

@@ -65,7 +65,9 @@ __device__ __forceinline__ int dg_kperm(int t, int h) {
   return ((t & 1) ? 3 : 0) ^ ((t & 2) ? 12 : 0) ^ ((h & 1) ? 1 : 0) ^ ((h & 2) ? 4 : 0);
 }
 
-template <bool TRANS>
+// SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
+// GEMM with no split arithmetic in its hot loop.
+template <bool TRANS, bool SPLIT = false>
 __global__ void __launch_bounds__(DG_THREADS, 1)
     dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const DGemmArgs g) {
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
-  const int split = g.k_split > 1 ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
+  const int split = SPLIT ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
   const int bid = (int)blockIdx.x - split * n_tiles * m_tiles;
   const int group = bid / (DG_GROUP_M * n_tiles);
   const int first_m = group * DG_GROUP_M;
@@ -91,9 +93,10 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   if (g.upper_only && m0 > n0 + DG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT_all = (g.K + DG_BK - 1) / DG_BK;
-  const int KTc = g.k_split > 1 ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
+  const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * DG_BK;
+  const int Krem = g.K - kbase;                    // K left from this split's first k
   const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       const int n = wn * DG_WN + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
     }
-    if (kbase + kt * DG_BK + k >= g.K) {
+    if (kt * DG_BK + k >= Krem) {
 #pragma unroll
       for (int mt = 0; mt < DG_MT; ++mt) f.a[mt][0] = f.a[mt][1] = 0.0;
 #pragma unroll

@@ -79,7 +79,9 @@ struct ZGemmArgs {
   long long split_ld;      //   and writes its partial product to out + s * split_ld (no beta)
 };
 
-template <bool CONJ>
+// SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
+// GEMM with no split arithmetic in its hot loop.
+template <bool CONJ, bool SPLIT = false>
 __global__ void __launch_bounds__(ZG_THREADS, 1)
     zgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const ZGemmArgs g) {
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
-  const int split = g.k_split > 1 ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
+  const int split = SPLIT ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
   const int bid = (int)blockIdx.x - split * n_tiles * m_tiles;
   const int group = bid / (ZG_GROUP_M * n_tiles);
   const int first_m = group * ZG_GROUP_M;
@@ -105,9 +107,10 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT_all = (g.K + ZG_BK - 1) / ZG_BK;
-  const int KTc = g.k_split > 1 ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
+  const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * ZG_BK;
+  const int Krem = g.K - kbase;                    // K left from this split's first k
   const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       const int n = wn * ZG_WN + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
     }
-    if (kbase + kt * ZG_BK + 8 * u + k >= g.K) {               // K tail (the TMA box may hold stale data)
+    if (kt * ZG_BK + 8 * u + k >= Krem) {               // K tail (the TMA box may hold stale data)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) f.a[mt][0] = f.a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
