@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
   const int split = SPLIT ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
-  const int bid = (int)blockIdx.x - split * n_tiles * m_tiles;
+  const unsigned bid = blockIdx.x - (unsigned)(split * n_tiles * m_tiles);
   const int group = bid / (ZG_GROUP_M * n_tiles);
   const int first_m = group * ZG_GROUP_M;
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
