@@ -17,6 +17,7 @@
 #include "dgemm.cuh"
 #include "eig.cuh"
 #include "hhqr.cuh"
+#include "gemm_tail.cuh"
 #include "qr_kernels.cuh"
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
@@ -138,6 +139,7 @@ struct chase_handle_s {
   char* c2ws = nullptr;     // solver: C2
   char* lanws = nullptr;    // solver: Lanczos basis
   char* hhws = nullptr;     // Householder QR fallback (see hh_layout)
+  char* tailws = nullptr;   // split-K tail partial tiles (gemm_tail.cuh)
   double* d_ritz = nullptr;
   double* d_nrm = nullptr;
   int* d_info = nullptr;
@@ -204,8 +206,9 @@ static int64_t pad_ld(int64_t rows) { return (rows + 1) & ~(int64_t)1; }
 
 static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
+constexpr int TAIL_TILES_MAX = 320;   // split-K tail: tiles x copies held (128 KB each)
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, hh, info, s, total;
+  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, hh, tail, info, s, total;
 };
 constexpr int LANCZOS_K = 25;       // Lanczos steps per run (bounds, Alg.1 l.2)
 constexpr int LANCZOS_RUNS = 4;     // independent runs pooled for the DoS estimate
@@ -276,6 +279,8 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)pad_ld(h->n_r) * (LANCZOS_K + 2) * es) + 4096;
   L.hh = off;                                           // Householder QR fallback
   off += hh_layout(h).total;
+  L.tail = off;                                         // split-K tail partial tiles
+  off += align256((size_t)TAIL_TILES_MAX * 128 * 128 * 8);
   L.info = off;
   off += 256;
   L.s = off;
@@ -291,10 +296,13 @@ static bool g_dfused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
-                                   const CUtensorMap& tX, const ZGemmArgs& a) {
+                                   const CUtensorMap& tX, const ZGemmArgs& a, int grid_tiles = 0) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
-  dim3 grid(((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM) * (split ? a.k_split : 1));
+  const int tiles = a.tail_tiles > 0 ? a.tail_tiles
+                    : grid_tiles > 0 ? grid_tiles
+                                     : ((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM);
+  dim3 grid(tiles * (split ? a.k_split : 1));
   static bool attr[2][2] = {{false, false}, {false, false}};
   auto go = [&](auto kern, bool& done) -> chase_status_t {
     if (!done) {
@@ -314,10 +322,13 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
                                          const FusedArgs& f, int T);
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
-                                   const CUtensorMap& tX, const DGemmArgs& a) {
+                                   const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
-  dim3 grid(((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM) * (split ? a.k_split : 1));
+  const int tiles = a.tail_tiles > 0 ? a.tail_tiles
+                    : grid_tiles > 0 ? grid_tiles
+                                     : ((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM);
+  dim3 grid(tiles * (split ? a.k_split : 1));
   static bool attr[2][2] = {{false, false}, {false, false}};
   auto go = [&](auto kern, bool& done) -> chase_status_t {
     if (!done) {
@@ -354,6 +365,8 @@ struct GemmReq {
   int64_t ldy2;
   int k_split;               // split-K copies (> 1: partial products at out + s * split_ld)
   int64_t split_ld;
+  int tail_tiles, tile_offset;  // split-K tail launch (see gemm_tail.cuh)
+  int grid_tiles;            // > 0: launch only the first grid_tiles tiles of the raster
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
@@ -371,7 +384,8 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.a3d = r.a3d;
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     a.k_split = r.k_split; a.split_ld = r.split_ld;
-    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a);
+    a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
+    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles);
   }
   DGemmArgs a;
   a.M = r.M; a.N = r.N; a.K = r.K;
@@ -386,7 +400,8 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.a3d = r.a3d;
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   a.k_split = r.k_split; a.split_ld = r.split_ld;
-  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a);
+  a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
+  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles);
 }
 
 static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
@@ -416,6 +431,69 @@ static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CU
     dgemm_fused_kernel<false><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
   }
   CUDA_TRY(cudaGetLastError());
+  return CHASE_OK;
+}
+
+// A big GEMM with its wave-quantisation tail split over K (gemm_tail.cuh): the plain kernel on
+// the first T_main tiles of the raster, the last T_tail tiles as S split-K copies into tile-local
+// partials, then the fixed-order sum + epilogue.  (T_tail, S) minimise the modelled waves
+// (equal-cost tiles, one CTA per SM); no split when nothing is gained.
+static chase_status_t run_gemm_tail(chase_handle_s* h, const GemmReq& g) {
+  static const bool off = getenv("CHASE_NO_TAIL_SPLIT") != nullptr;   // A/B switch
+  if (off || g.M <= 0 || g.N <= 0 || g.col_shift || g.diag_k || g.upper_only || g.abort_flag ||
+      g.k_split > 1 || !h->tailws)
+    return run_gemm(h, g);
+  const bool cplx = h->dt == CHASE_C128;
+  const int BM = cplx ? ZG_BM : DG_BM, BN = cplx ? ZG_BN : DG_BN, BK = cplx ? ZG_BK : DG_BK;
+  const int T = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int SMS = h->num_sms, KT = (g.K + BK - 1) / BK;
+  const int full = T / SMS, rem = T % SMS;
+  if (rem == 0) return run_gemm(h, g);
+  double best_gain = 0.02;                 // in waves; below this the split is not worth it
+  int bS = 1, btail = 0;
+  for (int extra = 0; extra <= std::min(1, full); ++extra) {
+    const int tail = rem + extra * SMS;
+    for (int S = 2; S <= 8; ++S) {
+      if (KT < 2 * S || S * tail > TAIL_TILES_MAX) break;
+      const int ktc = (KT + S - 1) / S;
+      if ((KT + ktc - 1) / ktc != S) continue;   // S copies must all be non-empty
+      const double waves = (double)((S * tail + SMS - 1) / SMS) / S;
+      const double gain = (extra + 1) - waves;
+      if (gain > best_gain) {
+        best_gain = gain;
+        bS = S;
+        btail = tail;
+      }
+    }
+  }
+  if (bS == 1) return run_gemm(h, g);
+  const int tmain = T - btail;
+  if (tmain > 0) {
+    GemmReq m = g;
+    m.grid_tiles = tmain;
+    STATUS_TRY(run_gemm(h, m));
+  }
+  GemmReq t = g;
+  t.k_split = bS;
+  t.tail_tiles = btail;
+  t.tile_offset = tmain;
+  t.out = h->tailws;
+  t.ldo = BM;
+  t.alpha = 1.0; t.beta = 0.0; t.c = 0.0; t.use_beta = 0;
+  t.band_lo = t.band_hi = 0; t.band_shift = 0; t.band_map = nullptr;
+  STATUS_TRY(run_gemm(h, t));
+  TailArgs ta{bS, btail, tmain, g.M, g.N, (long long)g.ldo, (long long)g.ldx, g.alpha, g.beta, g.c,
+              g.use_beta, g.band_lo, g.band_hi, g.band_shift, g.band_map};
+  if (cplx)
+    gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M><<<btail, 256, 0, h->stream>>>(
+        reinterpret_cast<const double2*>(h->tailws), static_cast<double2*>(g.out),
+        static_cast<const double2*>(g.xin), ta);
+  else
+    gemm_tail_epilogue_kernel<double, DG_BM, DG_BN, DG_GROUP_M><<<btail, 256, 0, h->stream>>>(
+        reinterpret_cast<const double*>(h->tailws), static_cast<double*>(g.out),
+        static_cast<const double*>(g.xin), ta);
+  CUDA_TRY(cudaGetLastError());
+  h->launches[g.conj ? CAT_HEMM_ODD : CAT_HEMM_EVEN] += 2;
   return CHASE_OK;
 }
 
@@ -713,6 +791,7 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
     delete h;
     return CHASE_ECUDA;
   }
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (p * q > 1) {
     ncclUniqueId uid;
     memcpy(&uid, id, 128);
@@ -785,6 +864,7 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->c2ws = base + L.c2;
   h->lanws = base + L.lan;
   h->hhws = base + L.hh;
+  h->tailws = base + L.tail;
   h->d_ritz = reinterpret_cast<double*>(base + L.ritz);
   h->d_nrm = reinterpret_cast<double*>(base + L.nrm);
   if (h->nb > 0) {
@@ -1055,7 +1135,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     }
     {
       ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
-      STATUS_TRY(run_gemm(h, g));
+      STATUS_TRY(run_gemm_tail(h, g));
     }
     if (fused) continue;                     // single-member communicator: nothing to reduce
     if (odd && h->p > 1) STATUS_TRY(allreduce(h, g.out, (size_t)ldb * r.k, h->ccomm));

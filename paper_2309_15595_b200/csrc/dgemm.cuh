@@ -59,6 +59,8 @@ struct DGemmArgs {
   long long ldy2;
   int k_split;             // split-K: see zgemm.cuh
   long long split_ld;
+  int tail_tiles;          // split-K tail of a big GEMM: see zgemm.cuh
+  int tile_offset;
 };
 
 __device__ __forceinline__ int dg_kperm(int t, int h) {
@@ -83,8 +85,10 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
-  const int split = SPLIT ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
-  const unsigned bid = blockIdx.x - (unsigned)(split * n_tiles * m_tiles);
+  const int tiles_launch = SPLIT && g.tail_tiles > 0 ? g.tail_tiles : n_tiles * m_tiles;
+  const int split = SPLIT ? (int)blockIdx.x / tiles_launch : 0;
+  const unsigned bid = SPLIT ? (unsigned)(g.tile_offset * (g.tail_tiles > 0) + (int)blockIdx.x - split * tiles_launch)
+                             : blockIdx.x;
   const int group = bid / (DG_GROUP_M * n_tiles);
   const int first_m = group * DG_GROUP_M;
   const int gm = min(DG_GROUP_M, m_tiles - first_m);
@@ -221,7 +225,10 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
           if (bsrc >= 0) v -= g.c * g.xin[(long long)bsrc + (long long)col * g.ldx];
           if (g.col_shift != nullptr) v -= g.col_shift[col] * g.y2[(long long)row + (long long)col * g.ldy2];
           v *= g.alpha;
-          double* o = g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
+          double* o = SPLIT && g.tail_tiles > 0
+                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (DG_BM * DG_BN) +
+                                 (row - m0) + (long long)(col - n0) * DG_BM
+                           : g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) v += g.beta * *o;
           *o = v;
         }

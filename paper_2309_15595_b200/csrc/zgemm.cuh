@@ -77,6 +77,10 @@ struct ZGemmArgs {
   long long ldy2;
   int k_split;             // > 1: split-K -- CTA blockIdx / tiles takes k-tiles [s KTc, (s+1) KTc)
   long long split_ld;      //   and writes its partial product to out + s * split_ld (no beta)
+  int tail_tiles;          // SPLIT, > 0: the launch covers only tiles [tile_offset, +tail_tiles)
+  int tile_offset;         //   of the raster (the wave-quantisation tail of a big GEMM), and each
+                           //   partial tile is stored tile-local: out + (s tail_tiles + j) BM BN,
+                           //   column-major with ld BM (gemm_tail_epilogue_kernel finishes them)
 };
 
 // SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
@@ -97,8 +101,10 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
   const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
-  const int split = SPLIT ? (int)blockIdx.x / (n_tiles * m_tiles) : 0;
-  const unsigned bid = blockIdx.x - (unsigned)(split * n_tiles * m_tiles);
+  const int tiles_launch = SPLIT && g.tail_tiles > 0 ? g.tail_tiles : n_tiles * m_tiles;
+  const int split = SPLIT ? (int)blockIdx.x / tiles_launch : 0;
+  const unsigned bid = SPLIT ? (unsigned)(g.tile_offset * (g.tail_tiles > 0) + (int)blockIdx.x - split * tiles_launch)
+                             : blockIdx.x;
   const int group = bid / (ZG_GROUP_M * n_tiles);
   const int first_m = group * ZG_GROUP_M;
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
@@ -292,7 +298,10 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           }
           vr *= g.alpha;
           vi *= g.alpha;
-          double2* o = g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
+          double2* o = SPLIT && g.tail_tiles > 0
+                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (ZG_BM * ZG_BN) +
+                                 (row - m0) + (long long)(col - n0) * ZG_BM
+                           : g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) {
             const double2 old = *o;
             vr += g.beta * old.x;

@@ -133,3 +133,16 @@ def test_residuals_match_oracle(complex_, N, n):
     torch.cuda.synchronize()
     h.close()
     assert np.max(np.abs(got - ref) / np.maximum(ref, 1e-300)) <= 1e-10
+
+
+@pytest.mark.parametrize("complex_,N,n", [(True, 2000, 600), (False, 4000, 600)])
+def test_filter_wave_tail_split(complex_, N, n):
+    """More output tiles than SMs with a remainder (complex 16 x 10 = 160 tiles, real 32 x 5 =
+    160): the plain GEMM runs the first 148 tiles, the last 12 run split over K with the
+    fixed-order tail epilogue (gemm_tail.cuh); ragged degrees shrink the tile grid step by step."""
+    A, V0, b = make_problem(N, n, complex_, 23)
+    degrees = sorted([2, 4, 6] * (n // 3))
+    ref, _ = oracle.chebyshev_filter(A, V0, degrees, b.c, b.e, b.mu_1)
+    out, st, _ = gpu_filter(A, V0, degrees, b, complex_)
+    assert st["matvecs"] == sum(degrees)
+    assert colwise_rel(out, ref) <= TOL
