@@ -224,3 +224,15 @@ def test_hhqr_fallback_paths():
         R = Q.conj().T @ X
         assert np.abs(np.tril(R, -1)).max() <= 1e-13 * np.abs(X).max()
         assert np.linalg.norm(Q @ R - X) <= 1e-13 * np.linalg.norm(X)
+
+
+def test_hhqr_row_permutation_invariance():
+    """Reading #33(c): the GPU HHQR takes rows in the "virtual" order of the column communicator
+    (rank 0's local rows, then rank 1's ...), a row permutation P of the block-cyclic global
+    order.  With diag(R) >= 0 the thin Q of P X is P Q (X full rank), so the order does not change
+    the result beyond rounding."""
+    X = ci.svd_synthesized(90, 12, 1e3, 21, True)
+    perm = np.concatenate([np.arange(k, 90, 3) for k in range(3)])      # cyclic-style dealing
+    Q = oracle.householder_qr(X)
+    Qp = oracle.householder_qr(X[perm])
+    assert np.abs(Qp - Q[perm]).max() <= 100 * 1e3 * 2.0 ** -53
