@@ -151,7 +151,6 @@ struct chase_handle_s {
   int world_size = 1;
   unsigned fused_ep = 0;
   unsigned long long fused_delivered = 0;
-  unsigned long long fused_ctr = 0;          // tile-scheduler counter value at the next launch
   int* d_err = nullptr;
   int num_sms = 148;
   // bookkeeping of the last filter call
@@ -935,7 +934,6 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
   h->d_err = reinterpret_cast<int*>(static_cast<char*>(local) + L.err);
   h->fused_ep = 0;
   h->fused_delivered = 0;
-  h->fused_ctr = 0;
   h->fused = true;
   return CHASE_OK;
 }

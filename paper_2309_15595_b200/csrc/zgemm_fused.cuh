@@ -45,7 +45,7 @@ struct FusedArgs {
   int* err;                                  // set on a spin timeout
   int plain;                                 // diagnostics: local epilogue, no protocol (m == 1)
   unsigned long long* tile_ctr;              // dynamic tile scheduler (monotonic, local)
-  unsigned long long ctr_base;               // value of *tile_ctr when this launch starts
+  unsigned long long ctr_base;               // value of *tile_ctr at launch start (0: reset per launch)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
