@@ -56,3 +56,28 @@ def test_uniform_1000(opt):
     assert np.all(r <= 2e-10)
     assert out["stats"]["b_sup"] >= lam[-1] - 1e-6          # Lanczos upper bound
     print(out["stats"])
+
+
+def test_hhqr_mode_same_convergence():
+    """"the usage of either HHQR or CholeskyQR results in the same convergence behaviour
+    with the same number of MatVec operations and iterations" (Table 3).  chase_set_qr_mode(h, 1)
+    runs Householder QR in every iteration; the run converges to the same eigenpairs in the same
+    number of iterations and matvecs as the Alg.4 (CholeskyQR) run."""
+    import torch
+    N, nev, nex = 600, 40, 20
+    lam = ci.uniform_spectrum(N)
+    A = ci.dense_from_spectrum(lam, 5, True)
+    res = {}
+    for mode in (0, 1):
+        h = cb.Chase(cb.CHASE_C128, N, nev + nex)
+        h.set_qr_mode(mode)
+        Ad = dev(A)
+        Vd = dev(np.zeros((N, nev + nex), dtype=A.dtype))
+        res[mode] = h.solve(Ad, Vd, nev, nex, tol=1e-10)
+        torch.cuda.synchronize()
+        h.close()
+    for mode in (0, 1):
+        assert res[mode]["status"] == 0, res[mode]
+        assert np.max(np.abs(res[mode]["lambda"][:nev] - lam[:nev])) <= 1e-9
+    assert res[0]["stats"]["iterations"] == res[1]["stats"]["iterations"]
+    assert res[0]["stats"]["matvecs"] == res[1]["stats"]["matvecs"]
