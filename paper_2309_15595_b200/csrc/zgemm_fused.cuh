@@ -3,23 +3,28 @@
 //
 // A filter step on a p x q grid is "partial_r = alpha (A_r^(H) X - c band) on every member r of
 // the row (even step) / column (odd step) communicator, then AllReduce(SUM)" (Alg.2 l.12).
-// Here every member runs a persistent grid (one CTA per SM, identical tile sequence on all
-// members).  After the K loop of output tile t a CTA
+// Here every member runs a persistent grid (one CTA per SM) over the step's output tiles, handed
+// out by a local dynamic tile scheduler.  After the K loop of output tile t a CTA
 //   1. pushes its partial tile into its slot of the tile owner's staging area (NVLink stores;
-//      the owner rotates along each CTA's tile sequence so owner work is spread evenly),
+//      the owner rotates with t / gridDim so owner work is spread evenly),
 //   2. releases a per-(tile, member) arrival flag in the owner's memory,
-// and, if it is the owner, waits for the m flags of t, sums the m partial tiles from its LOCAL
-// slots in fixed member order (deterministic, identical bits on every member), adds
-// beta * V_{s-2} (replicated, read locally), pushes the result into the output buffer of every
-// member and bumps each member's delivery counter.  The next step's kernel waits
+// and, if it owns t, queues t.  After every tile the CTA checks its queue without blocking: an
+// owned tile whose m flags are in is reduced -- the m partial tiles summed from its LOCAL slots
+// in fixed member order (deterministic, identical bits on every member), + beta * V_{s-2}
+// (replicated, read locally), pushed into the output buffer of every member, each member's
+// delivery counter bumped.  The CTA blocks only when its queue is full or at the end of its tile
+// stream, so a slower peer does not stall the owner's tensor pipe.  The next step's kernel waits
 // until its delivery counter covers the whole previous step.  The reduction traffic of tile t
-// overlaps the math of the tiles that follow it -- no separate collective launch.
+// overlaps the math of the tiles that follow it -- no separate collective launch.  Staging
+// slots and flags are separate per step parity: a rank's row and column communicators progress
+// independently, so a peer already in step s+1 must not touch what this rank still reads for s.
 //
 // The k-tile loads are refilled by the MMA warps in rotation (no producer warp); the tile id of
-// each sequence position is grabbed from the global counter two issue indices ahead.
-// Deadlock freedom: all CTAs are co-resident (grid <= #SMs, 1 CTA/SM) and every member walks the
-// same tile sequence per CTA; a partial is always published before its producer waits on
-// anything, so the wait at sequence position i only depends on positions <= i of the peers.
+// each sequence position is grabbed from the scheduler two issue indices ahead.
+// Deadlock freedom: all CTAs are co-resident (grid <= #SMs, 1 CTA/SM); a partial is always
+// published before its producer waits on anything; a blocked CTA waits on a tile no later than
+// its current one while every tile it holds ahead (prefetched) is later, so every chain of waits
+// decreases in tile index and ends at a CTA that is still computing.
 // Every spin is bounded (~10 s at 2 GHz); on timeout the kernel sets *err and gives up so a
 // broken peer can never hang the GPU.
 #pragma once
