@@ -466,8 +466,10 @@ def main():
             "filter_only_tflops": F * args.steps / (filt_ms / 1e3) / 1e12,
             "qr": {"variant": qr_info["variant"], "passes": qr_info["passes"],
                    "ms_per_step": (ms - filt_ms) / args.steps, "cond_est": est,
-                   "tflops": qr_flops(w, n, qr_info["passes"]) / n_gpus * args.steps /
-                             max(1e-9, (ms - filt_ms) / 1e3) / 1e12},
+                   # rows are split over the p ranks of a column communicator and the QR is
+                   # repeated in each of the q column communicators: per GPU = F / p
+                   "tflops_per_gpu": qr_flops(w, n, qr_info["passes"]) / p * args.steps /
+                                     max(1e-9, (ms - filt_ms) / 1e3) / 1e12},
             "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (HEMM step)" if w["complex_"] else "dgemm_kernel",
                          "achieved": hemm_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": hemm_achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
