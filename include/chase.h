@@ -62,13 +62,17 @@ typedef struct {
 } chase_bounds_t;
 
 /* Per-call statistics.  matvecs = sum_j d_j; steps = max degree D; qr_variant = the
- * Alg.4 branch actually executed; qr_passes = Gram/POTRF/TRSM rounds executed. */
+ * Alg.4 branch actually executed; qr_passes = Gram/POTRF/TRSM rounds executed;
+ * shift = the s = 11(mn + n(n+1)) u ||X||_F^2 of Alg.4 l.6 added to the Gram diagonal by
+ * the shifted pass (0 when no shifted pass ran), as computed on the device (norm = Re tr G,
+ * reading #12). */
 typedef struct {
   int64_t matvecs;
   int32_t steps;
   int32_t qr_variant;
   int32_t qr_passes;
   int32_t reserved;
+  double shift;
 } chase_stats_t;
 
 /* Bookkeeping record of one filter step s (1-based in the paper, index s-1 here):
@@ -128,6 +132,22 @@ chase_status_t chase_create_cyclic(chase_handle_t* h, chase_dtype_t dt, int64_t 
                                    int p, int q, int myrow, int mycol, int64_t nb,
                                    const uint8_t id[128], int device, void* cuda_stream);
 
+/* Virtual grid (tests and diagnostics): a handle for rank (myrow, mycol) of a
+ * p x q grid -- block (nb == 0) or block-cyclic -- whose ranks ALL live in this process on the
+ * same device, so the 2D distribution (bands of -cI, beta roles, C/B-layout alternation of P:149)
+ * and the fused multi-member reduction protocol run on one GPU.  No NCCL communicator is created:
+ * every filter step whose communicator has more than one member must run through the fused
+ * peer-memory path (chase_set_fused_workspace with peer_bases[r] = the region of virtual rank r,
+ * all on this device, and chase_set_fused_mode with an SM budget so the persistent kernels of
+ * all ranks are co-resident); each rank's chase_filter must be issued from its own host thread
+ * on its own stream (the call waits for its peers).  chase_filter without a fused workspace and
+ * every other collective call (chase_cholqr / chase_hhqr with p > 1, chase_residuals,
+ * chase_rayleigh_ritz, chase_solve) return CHASE_ESTATE on a virtual grid with p*q > 1.
+ * Errors as chase_create_cyclic. */
+chase_status_t chase_create_virtual(chase_handle_t* h, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                    int p, int q, int myrow, int mycol, int64_t nb, int device,
+                                    void* cuda_stream);
+
 /* Global indices of this rank's local rows (n_r entries) and columns (n_c entries), host
  * arrays; either may be NULL.  For the block distribution these are r0.. and c0.. */
 chase_status_t chase_local_indices(chase_handle_t h, int64_t* rows, int64_t* cols);
@@ -180,6 +200,14 @@ chase_status_t chase_fused_workspace_size(chase_handle_t h, size_t* bytes);
 chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const uint64_t* peer_bases,
                                          int world);
 
+/* Options of the fused path (host only).  mode 0 (default): the fused kernel runs for the steps
+ * whose communicator has more than one member; mode 1: every filter step runs it, single-member
+ * communicators (and 1 x 1 grids, world = 1, peer_bases[0] = local) included -- the protocol
+ * with itself, so the fused kernels can be exercised and measured on one GPU.
+ * sm_budget > 0 caps the persistent grid of a fused launch at that many CTAs (one per SM; e.g.
+ * #SMs / (p q) on a virtual grid); 0 = all SMs.  Errors: CHASE_EINVAL. */
+chase_status_t chase_set_fused_mode(chase_handle_t h, int32_t mode, int32_t sm_budget);
+
 /* ---------------------------------------------------------------------------------------
  * Chebyshev filter -- Eq.(1), Alg.1 l.4, Alg.2 l.12, with the
  * damped scalars of S:362 (reading #1):
@@ -204,11 +232,27 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
  *  c, e     centre and half-width of the damped interval [mu_ne, b_sup] (Alg.2 l.3).
  *  bounds   host: mu_1 sets the scaling point; mu_ne, b_sup informational (reading #2).
  *  stats    host, nullable: matvecs and steps.
- * Errors: CHASE_EINVAL, CHASE_EDEGREE, CHASE_EBOUNDS, CHASE_ESTATE (no workspace),
- * CHASE_ECUDA, CHASE_ENCCL.  Returns after enqueue. */
+ * Errors: CHASE_EINVAL, CHASE_EDEGREE, CHASE_EBOUNDS, CHASE_ESTATE (no workspace; or a fused
+ * handle after a peer timeout, until chase_set_fused_workspace is called again on every rank),
+ * CHASE_ECUDA, CHASE_ENCCL.  Returns after enqueue -- except with a fused workspace set, where
+ * the call copies V into and out of the symmetric region and synchronises the stream once at the
+ * end to read the peer-timeout flag (a timeout returns CHASE_ECUDA). */
 chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, void* V,
                             int64_t ldv, int64_t ncols, const int32_t* degrees, double c,
                             double e, const chase_bounds_t* bounds, chase_stats_t* stats);
+
+/* Diagnostics (tests): this rank's partial of ONE filter step, without the reduction -- the
+ * summand that rank (myrow, mycol) contributes to the AllReduce of P:149:
+ *   odd != 0: Y (n_c x k) = alpha (A_local^H X - c band(X)) + [use_beta] beta Y,  X n_r x k
+ *   odd == 0: Y (n_r x k) = alpha (A_local X - c band(X)) + [use_beta] beta Y,    X n_c x k
+ * band(X) = the rows of X on this rank's share of the diagonal (reading #6; block-cyclic: the
+ * per-row maps), exactly as chase_filter applies it; the same kernels as chase_filter's local
+ * steps.  X and Y device, column-major, must not overlap; ldx/ldy >= their row counts, 16-byte
+ * pitch for X.  Works on real and virtual handles.  Errors: CHASE_EINVAL, CHASE_ESTATE,
+ * CHASE_ECUDA.  Returns after enqueue. */
+chase_status_t chase_filter_step(chase_handle_t h, const void* A_local, int64_t lda, const void* X,
+                                 int64_t ldx, void* Y, int64_t ldy, int64_t k, int32_t odd,
+                                 double alpha, double beta, double c, int32_t use_beta);
 
 /* The per-step record of the last chase_filter call on this handle (the schedule that was
  * actually launched).  rec: host array of max_steps entries; *nsteps = D. */
@@ -249,7 +293,8 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
 /* ---------------------------------------------------------------------------------------
  * Householder QR -- Alg.4 l.9 "X <- ScaLAPACK-HHQR(X, comm)" on the GPU:
  * blocked Householder QR of the C-layout block over the rows of the column communicator
- * (xGEQRF order, 32-wide panels as the paper's ScaLAPACK column block; reflectors of
+ * (xGEQRF order, 128-wide panels -- the paper's ScaLAPACK run used a 32-column block, P:448,
+ * reading #33d; reflectors of
  * LAPACK xLARFG; compact-WY trailing updates on the tensor-core GEMMs; AllReduce over ccomm
  * per column and per panel), then the thin Q (xUNGQR order), written back into V with column
  * j scaled by sign(R_jj) so diag(R) is non-negative (reading #33).  Never fails on rank
@@ -300,7 +345,8 @@ chase_status_t chase_solve(chase_handle_t h, const void* A_local, int64_t lda, v
  *  ritz    host out: the ncols Ritz values, ascending (V's columns in the same order).
  *  sweeps  host out, nullable: Jacobi sweeps used (convergence: off(A) <= 1e-14 ||A||_F).
  * Uses the B-layout, Gram and eigensolver workspace.  Synchronises the stream once per sweep.
- * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL. */
+ * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL, CHASE_ENOCONV (the Jacobi
+ * solver did not reach its off-norm test within 40 sweeps; the results are written anyway). */
 chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_t lda, void* V,
                                    int64_t ldv, int64_t ncols, double* ritz, int32_t* sweeps);
 

@@ -19,6 +19,6 @@ from .filter import chebyshev_scalars, chebyshev_filter, filter_schedule, filter
 from .qr import (gram, potrf_upper, trsm_right_upper, shift_value, cholesky_qr, caqr,  # noqa: F401
                  cond_est, select_variant, householder_qr, householder_factor, larfg,
                  frobenius_sq)
-from .grid import distributed_filter  # noqa: F401
+from .grid import distributed_filter, step_partial  # noqa: F401
 from .residual import residuals  # noqa: F401
 from .rayleigh_ritz import rayleigh_ritz  # noqa: F401

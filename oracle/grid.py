@@ -39,6 +39,29 @@ def _owned(N, P, k, nb):
     return g[(g // nb) % P == k]
 
 
+def step_partial(A, X, Y_old, i, j, p, q, odd, alpha, beta, c, use_beta, nb=0):
+    """The summand rank (i, j) contributes to the AllReduce of one filter step:
+        odd:  alpha (A_ij^H X - c band_ij(X)) + [use_beta] beta Y_old     (X = C_i, Y = B_j)
+        even: alpha (A_ij X  - c band_ij(X)) + [use_beta] beta Y_old      (X = B_j, Y = C_i)
+    band_ij(X) = the rows of X whose global index is both a row of grid row i and a column of
+    grid column j (reading #6), placed on the output rows of the same global index."""
+    N = A.shape[0]
+    ri, cj = _owned(N, p, i, nb), _owned(N, q, j, nb)
+    Aij = A[np.ix_(ri, cj)]
+    if odd:
+        part = Aij.conj().T @ X
+        # diagonal share: B rows (global cj) that are also local C rows (global ri)
+        _, o_out, o_in = np.intersect1d(cj, ri, return_indices=True)
+    else:
+        part = Aij @ X
+        _, o_out, o_in = np.intersect1d(ri, cj, return_indices=True)
+    part[o_out] -= c * X[o_in]
+    part = alpha * part
+    if use_beta:
+        part = part + beta * Y_old
+    return part
+
+
 def distributed_filter(A, V0, degrees, c, e, mu_1, p, q, nb=0):
     """nb > 0: block-cyclic distribution; the diagonal share of rank (i, j) is then the set of
     global indices owned both as a row (grid row i) and as a column (grid column j)."""
@@ -57,30 +80,17 @@ def distributed_filter(A, V0, degrees, c, e, mu_1, p, q, nb=0):
         if s % 2 == 1:
             for j, cj in enumerate(Cc):
                 acc = None
-                for i, ri in enumerate(R):
-                    Aij = A[np.ix_(ri, cj)]
-                    Ci = C[i][:, off:]
-                    part = Aij.conj().T @ Ci
-                    # diagonal share: B rows (global cj) that are also local C rows (global ri)
-                    _, ob, oc = np.intersect1d(cj, ri, return_indices=True)
-                    part[ob] -= c * Ci[oc]
-                    part = alpha[s - 1] * part
-                    if i == 0 and s > 1:
-                        part = part + beta[s - 1] * B[j][:, off:]
+                for i in range(p):
+                    part = step_partial(A, C[i][:, off:], B[j][:, off:], i, j, p, q, True,
+                                        alpha[s - 1], beta[s - 1], c, i == 0 and s > 1, nb)
                     acc = part if acc is None else acc + part
                 B[j][:, off:] = acc
         else:
             for i, ri in enumerate(R):
                 acc = None
-                for j, cj in enumerate(Cc):
-                    Aij = A[np.ix_(ri, cj)]
-                    Bj = B[j][:, off:]
-                    part = Aij @ Bj
-                    _, oc, ob = np.intersect1d(ri, cj, return_indices=True)
-                    part[oc] -= c * Bj[ob]
-                    part = alpha[s - 1] * part
-                    if j == 0:
-                        part = part + beta[s - 1] * C[i][:, off:]
+                for j in range(q):
+                    part = step_partial(A, B[j][:, off:], C[i][:, off:], i, j, p, q, False,
+                                        alpha[s - 1], beta[s - 1], c, j == 0, nb)
                     acc = part if acc is None else acc + part
                 C[i][:, off:] = acc
     out = np.empty((N, n), dtype=dtype)

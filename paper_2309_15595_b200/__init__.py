@@ -36,7 +36,7 @@ EXPORTED = (
     "chase_status_string", "chase_residuals", "chase_fused_workspace_size",
     "chase_set_fused_workspace", "chase_create_cyclic", "chase_local_indices",
     "chase_cyclic_indices", "chase_rayleigh_ritz", "chase_solve", "chase_hhqr",
-    "chase_set_qr_mode",
+    "chase_set_qr_mode", "chase_create_virtual", "chase_set_fused_mode", "chase_filter_step",
 )
 
 
@@ -53,7 +53,7 @@ class chase_bounds_t(ctypes.Structure):
 class chase_stats_t(ctypes.Structure):
     _fields_ = [("matvecs", ctypes.c_int64), ("steps", ctypes.c_int32),
                 ("qr_variant", ctypes.c_int32), ("qr_passes", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("reserved", ctypes.c_int32), ("shift", ctypes.c_double)]
 
 
 class chase_solve_stats_t(ctypes.Structure):
@@ -86,6 +86,9 @@ def load() -> ctypes.CDLL:
         "chase_create": (I32, [ctypes.POINTER(V), I32, I64, I64, I32, I32, I32, I32, ctypes.c_char_p, I32, V]),
         "chase_set_stream": (I32, [V, V]),
         "chase_create_cyclic": (I32, [ctypes.POINTER(V), I32, I64, I64, I32, I32, I32, I32, I64, ctypes.c_char_p, I32, V]),
+        "chase_create_virtual": (I32, [ctypes.POINTER(V), I32, I64, I64, I32, I32, I32, I32, I64, I32, V]),
+        "chase_set_fused_mode": (I32, [V, I32, I32]),
+        "chase_filter_step": (I32, [V, V, I64, V, I64, V, I64, I64, I32, D, D, D, I32]),
         "chase_local_indices": (I32, [V, c_i64p, c_i64p]),
         "chase_cyclic_indices": (I32, [I64, I32, I32, I64, c_i64p, c_i64p]),
         "chase_local_dims": (I32, [V, c_i64p, c_i64p, c_i64p, c_i64p]),
@@ -162,10 +165,14 @@ def chase_get_unique_id() -> bytes:
 
 def chase_create(dtype: int, N: int, n_max: int, p: int = 1, q: int = 1, myrow: int = 0,
                  mycol: int = 0, uid: bytes | None = None, device: int = 0, stream: int = 0,
-                 nb: int = 0):
-    """nb > 0: block-cyclic distribution with block size nb (chase_create_cyclic)."""
+                 nb: int = 0, virtual: bool = False):
+    """nb > 0: block-cyclic distribution with block size nb (chase_create_cyclic).
+    virtual: a rank of a grid living in this process on one device (chase_create_virtual)."""
     h = ctypes.c_void_p()
-    if nb:
+    if virtual:
+        _check(load().chase_create_virtual(ctypes.byref(h), dtype, N, n_max, p, q, myrow, mycol, nb,
+                                           device, ctypes.c_void_p(stream)), "chase_create_virtual")
+    elif nb:
         _check(load().chase_create_cyclic(ctypes.byref(h), dtype, N, n_max, p, q, myrow, mycol, nb,
                                           uid, device, ctypes.c_void_p(stream)), "chase_create_cyclic")
     else:
@@ -236,6 +243,24 @@ def chase_set_fused_workspace(h, local_ptr: int | None, peer_ptrs=None):
            "chase_set_fused_workspace")
 
 
+def chase_set_fused_mode(h, mode: int, sm_budget: int = 0):
+    """mode 1: every filter step runs the fused kernel (also single-member communicators);
+    sm_budget > 0: cap on the persistent fused grid (include/chase.h)."""
+    _check(load().chase_set_fused_mode(h, int(mode), int(sm_budget)), "chase_set_fused_mode")
+
+
+def chase_filter_step(h, A_local, X, Y, odd: bool, alpha: float, beta: float, c: float,
+                      use_beta: bool, k: int | None = None):
+    """This rank's partial of one filter step into Y, no reduction (include/chase.h)."""
+    a_ptr, lda = _colmajor(A_local, "A_local")
+    x_ptr, ldx = _colmajor(X, "X")
+    y_ptr, ldy = _colmajor(Y, "Y")
+    k = X.shape[1] if k is None else k
+    _check(load().chase_filter_step(h, a_ptr, lda, x_ptr, ldx, y_ptr, ldy, k, 1 if odd else 0,
+                                    float(alpha), float(beta), float(c), 1 if use_beta else 0),
+           "chase_filter_step")
+
+
 def chase_filter(h, A_local, V, degrees, c: float, e: float, bounds, ncols: int | None = None):
     """Chebyshev filter in place on V (see include/chase.h).  bounds = (mu_1, mu_ne, b_sup)."""
     a_ptr, lda = _colmajor(A_local, "A_local")
@@ -290,7 +315,8 @@ def chase_cholqr(h, V, cond_est: float, ncols: int | None = None, raise_on_error
     s = load().chase_cholqr(h, v_ptr, ldv, ncols, float(cond_est), ctypes.byref(st), ctypes.byref(info))
     if raise_on_error:
         _check(s, "chase_cholqr")
-    return {"status": s, "variant": st.qr_variant, "passes": st.qr_passes, "info": info.value}
+    return {"status": s, "variant": st.qr_variant, "passes": st.qr_passes, "info": info.value,
+            "shift": st.shift}
 
 
 def chase_hhqr(h, V, ncols: int | None = None):
@@ -396,12 +422,14 @@ class Chase:
     """One handle + its torch-owned workspace (a rank of the p x q grid, one GPU)."""
 
     def __init__(self, dtype: int, N: int, n_max: int, p: int = 1, q: int = 1, myrow: int = 0,
-                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream=None, nb: int = 0):
+                 mycol: int = 0, uid: bytes | None = None, device: int = 0, stream=None, nb: int = 0,
+                 virtual: bool = False):
         import torch
         self.device = torch.device("cuda", device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.stream = s
-        self.h = chase_create(dtype, N, n_max, p, q, myrow, mycol, uid, device, s.cuda_stream, nb)
+        self.h = chase_create(dtype, N, n_max, p, q, myrow, mycol, uid, device, s.cuda_stream, nb,
+                              virtual)
         self.n_r, self.n_c, self.r0, self.c0 = chase_local_dims(self.h)
         self.rows, self.cols = chase_local_indices(self.h, self.n_r, self.n_c)
         nbytes = chase_workspace_size(self.h)
@@ -411,6 +439,9 @@ class Chase:
 
     def filter(self, A_local, V, degrees, c, e, bounds, ncols=None):
         return chase_filter(self.h, A_local, V, degrees, c, e, bounds, ncols)
+
+    def filter_step(self, A_local, X, Y, odd, alpha, beta, c, use_beta, k=None):
+        return chase_filter_step(self.h, A_local, X, Y, odd, alpha, beta, c, use_beta, k)
 
     def cholqr(self, V, cond_est, ncols=None, raise_on_error=True):
         return chase_cholqr(self.h, V, cond_est, ncols, raise_on_error)

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "chase.h"
@@ -145,8 +146,16 @@ struct chase_handle_s {
   int* d_info = nullptr;
   double* d_shift = nullptr;
   int* h_info = nullptr;    // pinned
+  double* h_shift = nullptr;   // pinned: the shift of the last shifted CholeskyQR pass
+  double last_shift = 0.0;
+  // virtual grid (chase_create_virtual): every rank of the grid lives in this process on one
+  // device, no NCCL communicators; reductions only through the fused peer-memory path
+  bool virt = false;
   // fused compute+collective filter (symmetric peer memory); see zgemm_fused.cuh
   bool fused = false;
+  int fused_mode = 0;             // 1: single-member steps also run the fused kernel (self)
+  int sm_budget = 0;              // > 0: persistent fused grids use at most this many CTAs
+  bool fused_broken = false;      // a peer wait timed out: chase_set_fused_workspace again
   char* fz_base[FUSED_MAX_MEMBERS * FUSED_MAX_MEMBERS] = {nullptr};   // per world rank
   int world_size = 1;
   unsigned fused_ep = 0;
@@ -415,7 +424,7 @@ static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CU
   a.use_beta = 0; a.band_lo = r.band_lo; a.band_hi = r.band_hi; a.band_shift = r.band_shift;
   a.band_map = r.band_map;
   a.a3d = r.a3d;
-  const int grid = std::min(T, h->num_sms);
+  const int grid = std::min(T, h->sm_budget > 0 ? std::min(h->sm_budget, h->num_sms) : h->num_sms);
   if (trans) {
     if (!g_dfused_attr[1]) {
       CUDA_TRY(cudaFuncSetAttribute(dgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
@@ -510,7 +519,7 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
   a.use_beta = 0; a.band_lo = r.band_lo; a.band_hi = r.band_hi; a.band_shift = r.band_shift;
   a.band_map = r.band_map;
   a.a3d = r.a3d;
-  const int grid = std::min(T, h->num_sms);
+  const int grid = std::min(T, h->sm_budget > 0 ? std::min(h->sm_budget, h->num_sms) : h->num_sms);
   if (conj) {
     if (!g_fused_attr[1]) {
       CUDA_TRY(cudaFuncSetAttribute(zgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
@@ -649,6 +658,46 @@ static FusedLayout fused_layout(const chase_handle_s* h) {
   return L;
 }
 
+// ==================================================================== kernel preloading
+// Load (and size the dynamic shared memory of) every kernel of the filter and CholeskyQR paths
+// once per process, before the first launch.  Under CUDA lazy module loading the first launch
+// of a kernel loads its module and may wait for the device to go idle; a fused kernel spinning
+// on a peer that is itself blocked in such a load (several ranks of a virtual grid in one
+// process) would wait for nothing until its timeout, and a first-use load inside a timed
+// region would be charged to it.
+static chase_status_t preload_kernels() {
+  static std::once_flag once;
+  static chase_status_t status = CHASE_OK;
+  std::call_once(once, [] {
+    auto smem = [](const void* k, int bytes) {
+      cudaFuncAttributes a;
+      if (cudaFuncGetAttributes(&a, k) != cudaSuccess) return false;
+      return bytes == 0 || cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
+    };
+    bool ok = true;
+    ok &= smem((const void*)zgemm_kernel<true>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)zgemm_kernel<false>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)zgemm_kernel<true, true>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)zgemm_kernel<false, true>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<true>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<false>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<true, true>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<false, true>, DG_SMEM_BYTES);
+    ok &= smem((const void*)zgemm_fused_kernel<true>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)zgemm_fused_kernel<false>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_fused_kernel<true>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_fused_kernel<false>, DG_SMEM_BYTES);
+    ok &= smem((const void*)fused_wait_kernel, 0);
+    ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN, DG_GROUP_M>, 0);
+    if (!ok) {
+      fprintf(stderr, "[chase] kernel preload failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+      status = CHASE_ECUDA;
+    }
+  });
+  return status;
+}
+
 // ==================================================================== schedule (pure)
 static chase_status_t validate_degrees(int64_t ncols, const int32_t* degrees) {
   if (!degrees) return CHASE_EINVAL;
@@ -742,9 +791,11 @@ chase_status_t chase_create(chase_handle_t* out, chase_dtype_t dt, int64_t N, in
   return chase_create_cyclic(out, dt, N, n_max, p, q, myrow, mycol, 0, id, device, cuda_stream);
 }
 
-chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
-                                   int p, int q, int myrow, int mycol, int64_t nb,
-                                   const uint8_t id[128], int device, void* cuda_stream) {
+}  // extern "C"
+
+static chase_status_t create_handle(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                    int p, int q, int myrow, int mycol, int64_t nb,
+                                    const uint8_t id[128], int device, void* cuda_stream, bool virt) {
   if (!out) return CHASE_EINVAL;
   if (nb < 0) return CHASE_EINVAL;
   *out = nullptr;
@@ -752,8 +803,9 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
   if (N < 1 || n_max < 1 || n_max > N || N > (int64_t)INT32_MAX) return CHASE_EINVAL;
   if (p < 1 || q < 1 || myrow < 0 || myrow >= p || mycol < 0 || mycol >= q) return CHASE_EINVAL;
   if (p > N || q > N) return CHASE_EINVAL;
-  if (p * q > 1 && !id) return CHASE_EINVAL;
+  if (p * q > 1 && !id && !virt) return CHASE_EINVAL;
   chase_handle_s* h = new chase_handle_s();
+  h->virt = virt;
   h->dt = dt;
   h->N = N;
   h->n_max = n_max;
@@ -786,12 +838,17 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
   }
   h->device = device;
   h->stream = static_cast<cudaStream_t>(cuda_stream);
-  if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&h->h_info, sizeof(int)) != cudaSuccess) {
+  if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&h->h_info, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&h->h_shift, sizeof(double)) != cudaSuccess) {
     delete h;
     return CHASE_ECUDA;
   }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (p * q > 1) {
+  if (preload_kernels() != CHASE_OK) {
+    chase_destroy(h);
+    return CHASE_ECUDA;
+  }
+  if (p * q > 1 && !virt) {
     ncclUniqueId uid;
     memcpy(&uid, id, 128);
     const int rank = myrow * q + mycol;
@@ -805,6 +862,27 @@ chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_
     }
   }
   *out = h;
+  return CHASE_OK;
+}
+
+extern "C" {
+
+chase_status_t chase_create_cyclic(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                   int p, int q, int myrow, int mycol, int64_t nb,
+                                   const uint8_t id[128], int device, void* cuda_stream) {
+  return create_handle(out, dt, N, n_max, p, q, myrow, mycol, nb, id, device, cuda_stream, false);
+}
+
+chase_status_t chase_create_virtual(chase_handle_t* out, chase_dtype_t dt, int64_t N, int64_t n_max,
+                                    int p, int q, int myrow, int mycol, int64_t nb, int device,
+                                    void* cuda_stream) {
+  return create_handle(out, dt, N, n_max, p, q, myrow, mycol, nb, nullptr, device, cuda_stream, true);
+}
+
+chase_status_t chase_set_fused_mode(chase_handle_t h, int32_t mode, int32_t sm_budget) {
+  if (!h || (mode != 0 && mode != 1) || sm_budget < 0) return CHASE_EINVAL;
+  h->fused_mode = mode;
+  h->sm_budget = sm_budget;
   return CHASE_OK;
 }
 
@@ -915,6 +993,7 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
   if (!h) return CHASE_EINVAL;
   if (!local) {
     h->fused = false;
+    h->fused_broken = false;
     return CHASE_OK;
   }
   if (world != h->p * h->q || !peer_bases || world > 64) return CHASE_EINVAL;
@@ -934,6 +1013,7 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
   h->d_err = reinterpret_cast<int*>(static_cast<char*>(local) + L.err);
   h->fused_ep = 0;
   h->fused_delivered = 0;
+  h->fused_broken = false;
   h->fused = true;
   return CHASE_OK;
 }
@@ -1010,10 +1090,12 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
   const int64_t n_r = h->n_r, n_c = h->n_c;
   // working buffers: NCCL mode filters V in place and uses the B workspace; fused mode runs in
   // the symmetric region (peers write their reduced tiles straight into it)
-  // CHASE_FUSED_SELF=1: run the fused kernel even for single-member steps (diagnostics: measures
-  // the persistent kernel + epilogue protocol without any peer)
-  static const bool fused_self = getenv("CHASE_FUSED_SELF") != nullptr;
+  // fused_mode 1 (chase_set_fused_mode): the fused kernel runs even for single-member steps
+  // (its protocol with itself; makes the fused kernels testable on one GPU)
+  const bool fused_self = h->fused_mode == 1;
   const bool fused = h->fused && (h->p > 1 || h->q > 1 || fused_self);
+  if (h->fused && h->fused_broken) return CHASE_ESTATE;     // re-run chase_set_fused_workspace
+  if (h->virt && !fused && h->p * h->q > 1) return CHASE_ESTATE;   // no NCCL on a virtual grid
   FusedLayout FL{};
   char* Cbuf = static_cast<char*>(V);
   int64_t ldc = ldv;
@@ -1155,7 +1237,10 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     CUDA_TRY(cudaMemcpyAsync(h->h_info, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (*h->h_info != 0) {
+      // the delivery counters no longer match h->fused_delivered on every member: the handle
+      // refuses further fused calls until chase_set_fused_workspace re-zeroes them collectively
       fprintf(stderr, "[chase] fused filter: peer wait timed out\n");
+      h->fused_broken = true;
       return CHASE_ECUDA;
     }
   }
@@ -1166,6 +1251,47 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     stats->steps = D;
   }
   return CHASE_OK;
+}
+
+// Diagnostics: this rank's partial of one filter step, no reduction (include/chase.h).
+chase_status_t chase_filter_step(chase_handle_t h, const void* A_local, int64_t lda, const void* X,
+                                 int64_t ldx, void* Y, int64_t ldy, int64_t k, int32_t odd,
+                                 double alpha, double beta, double c, int32_t use_beta) {
+  if (!h || !A_local || !X || !Y) return CHASE_EINVAL;
+  if (k < 1 || k > h->n_max || lda < h->n_r) return CHASE_EINVAL;
+  const int64_t rows_in = odd ? h->n_r : h->n_c, rows_out = odd ? h->n_c : h->n_r;
+  if (ldx < rows_in || ldy < rows_out) return CHASE_EINVAL;
+  if (!std::isfinite(alpha) || !std::isfinite(beta) || !std::isfinite(c)) return CHASE_EINVAL;
+  if (!h->ws) return CHASE_ESTATE;
+  const size_t es = esize_of(h->dt);
+  if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(X) & 15) ||
+      (reinterpret_cast<uintptr_t>(Y) & 15))
+    return CHASE_EINVAL;
+  if (((size_t)lda * es) % 16 || ((size_t)ldx * es) % 16) return CHASE_EINVAL;
+  // the band of this rank (reading #6), exactly as build_schedule records it
+  std::vector<chase_step_record_t> rec;
+  int64_t mv;
+  const int32_t degs2[1] = {2};
+  build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol, h->nb}, 1, degs2, &rec, &mv);
+  const chase_step_record_t& r = rec[odd ? 0 : 1];
+  CUtensorMap tA, tX;
+  int a3d = 0;
+  STATUS_TRY(make_role_map(h, &tA, A_local, h->n_r, h->n_c, lda, odd ? ROLE_A_TRANS : ROLE_A_NOTRANS,
+                           odd ? nullptr : &a3d));
+  STATUS_TRY(make_role_map(h, &tX, X, rows_in, k, ldx, ROLE_X));
+  GemmReq g{};
+  g.conj = odd != 0;
+  g.tA = &tA; g.tX = &tX; g.a3d = a3d;
+  g.M = (int)rows_out; g.N = (int)k; g.K = (int)rows_in;
+  g.out = Y; g.ldo = ldy;
+  g.xin = X; g.ldx = ldx;
+  g.alpha = alpha; g.beta = beta; g.c = c;
+  g.use_beta = use_beta ? 1 : 0;
+  g.band_lo = r.band_lo; g.band_hi = r.band_hi;
+  g.band_shift = odd ? (int)(h->c0 - h->r0) : (int)(h->r0 - h->c0);
+  g.band_map = h->nb > 0 ? (odd ? h->d_band_odd : h->d_band_even) : nullptr;
+  ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
+  return run_gemm_tail(h, g);
 }
 
 }  // extern "C"
@@ -1245,9 +1371,12 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
       }
     }
     CUDA_TRY(cudaMemcpyAsync(h->h_info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    if (shifted)
+      CUDA_TRY(cudaMemcpyAsync(h->h_shift, h->d_shift, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   *info = *h->h_info;
+  if (shifted) h->last_shift = *h->h_shift;
   if (*info != 0) return CHASE_ECHOL;
   // TRSM V <- V R^{-1}, Alg.3 l.6: right-looking blocked with inverted 64x64 diagonal blocks.
   // Solved block columns go to W (W_k = V_k Rinv_kk), the trailing columns of V are updated
@@ -1324,7 +1453,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
   if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;   // TMA pitch
   if (!(cond_est >= 1.0)) return CHASE_EINVAL;   // also rejects NaN
-  if (!h->ws) return CHASE_ESTATE;
+  if (!h->ws || (h->virt && h->p > 1)) return CHASE_ESTATE;
   if (reinterpret_cast<uintptr_t>(V) & 15) return CHASE_EINVAL;
   if (!g_qr_attr_done) {
     CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double2>()));
@@ -1348,6 +1477,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   // Alg.4: est > 1e8 -> shifted CholeskyQR2; est < 20 -> CholeskyQR; else CholeskyQR2
   int variant = cond_est > 1e8 ? CHASE_QR_SHIFTED : (cond_est < 20.0 ? CHASE_QR_CHOL1 : CHASE_QR_CHOL2);
   int info = 0, passes = 0;
+  h->last_shift = 0.0;
   chase_status_t st = CHASE_OK;
   bool hh = h->qr_mode == 1;                     // HHQR in every call (Table 3)
   if (!hh && variant != CHASE_QR_SHIFTED) {
@@ -1384,6 +1514,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   if (stats) {
     stats->qr_variant = variant;
     stats->qr_passes = passes;
+    stats->shift = h->last_shift;
   }
   if (info_out) *info_out = info;
   return st;
@@ -1394,7 +1525,7 @@ chase_status_t chase_hhqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols)
   if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
   if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;
   if (reinterpret_cast<uintptr_t>(V) & 15) return CHASE_EINVAL;
-  if (!h->ws) return CHASE_ESTATE;
+  if (!h->ws || (h->virt && h->p > 1)) return CHASE_ESTATE;
   return hhqr_run(h, V, ldv, (int)ncols);
 }
 
@@ -1481,7 +1612,7 @@ chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t ld
   if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
   for (int64_t j = 0; j < ncols; ++j)
     if (!std::isfinite(ritz[j])) return CHASE_EINVAL;
-  if (!h->ws) return CHASE_ESTATE;
+  if (!h->ws || (h->virt && h->p * h->q > 1)) return CHASE_ESTATE;
   const size_t es = esize_of(h->dt), per = es / 8;
   if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
     return CHASE_EINVAL;
@@ -1538,7 +1669,7 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
                                    int64_t ldv, int64_t ncols, double* ritz, int32_t* sweeps_out) {
   if (!h || !A_local || !V || !ritz) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
-  if (!h->ws) return CHASE_ESTATE;
+  if (!h->ws || (h->virt && h->p * h->q > 1)) return CHASE_ESTATE;
   const size_t es = esize_of(h->dt);
   if ((reinterpret_cast<uintptr_t>(A_local) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
     return CHASE_EINVAL;
@@ -1677,6 +1808,7 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
   // fastest: n = 3000 in 13 sweeps, 2.0 s vs 2.8 s with inner convergence)
   static const int inner_sweeps = getenv("CHASE_JAC_INNER") ? atoi(getenv("CHASE_JAC_INNER")) : 1;
   std::vector<double> off(2);
+  bool converged = false;
   for (; sweeps < max_sweeps; ++sweeps) {
     for (int r = 0; r < (L > 2 ? R : 1); ++r) {
       jacobi_pair_kernel<<<(unsigned)(np / JAC_PW), JAC_THREADS, JAC_SMEM, h->stream>>>(Abuf[cur], np, Ubd, np, inner_sweeps);
@@ -1693,6 +1825,7 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (!(off[0] > 1e-28 * off[1])) {
       ++sweeps;
+      converged = true;
       break;
     }
   }
@@ -1736,7 +1869,10 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
   CUDA_TRY(cudaMemcpy2DAsync(V, ldv * es, W, ldw * es, n_r * es, n, cudaMemcpyDeviceToDevice, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (sweeps_out) *sweeps_out = sweeps;
-  return CHASE_OK;
+  if (!converged)
+    fprintf(stderr, "[chase] rayleigh_ritz: Jacobi not converged after %d sweeps (off %.3e, ||A|| %.3e)\n",
+            sweeps, std::sqrt(off[0]), std::sqrt(off[1]));
+  return converged ? CHASE_OK : CHASE_ENOCONV;
 }
 
 double chase_shift_value(int64_t m, int64_t n, double norm) {
@@ -1795,6 +1931,7 @@ chase_status_t chase_destroy(chase_handle_t h) {
   }
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->h_info) cudaFreeHost(h->h_info);
+  if (h->h_shift) cudaFreeHost(h->h_shift);
   delete h;
   return CHASE_OK;
 }

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       if (threadIdx.x == 0) atomicAdd(f.done[f.me], 1ull);
       return;
     }
-    const int owner = (t / (int)gridDim.x) % f.m;
+    const int owner = t % f.m;
     double* slot = reinterpret_cast<double*>(f.P[owner]) + (long long)f.me * f.slot;
 #pragma unroll
     for (int mt = 0; mt < DG_MT; ++mt)

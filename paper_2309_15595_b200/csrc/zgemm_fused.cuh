@@ -6,7 +6,8 @@
 // Here every member runs a persistent grid (one CTA per SM) over the step's output tiles, handed
 // out by a local dynamic tile scheduler.  After the K loop of output tile t a CTA
 //   1. pushes its partial tile into its slot of the tile owner's staging area (NVLink stores;
-//      the owner rotates with t / gridDim so owner work is spread evenly),
+//      owner = t mod m: the tiles in flight at any moment (consecutive ids from the dynamic
+//      scheduler) spread their partials and broadcasts over all members' NVLink ports),
 //   2. releases a per-(tile, member) arrival flag in the owner's memory,
 // and, if it owns t, queues t.  After every tile the CTA checks its queue without blocking: an
 // owned tile whose m flags are in is reduced -- the m partial tiles summed from its LOCAL slots
@@ -354,8 +355,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       if (threadIdx.x == 0) atomicAdd(f.done[f.me], 1ull);
       return;
     }
-    // owner rotates along the CTA's tile sequence (t / gridDim) so every CTA owns 1/m of its tiles
-    const int owner = (t / (int)gridDim.x) % f.m;
+    // owner = t mod m: consecutive tiles (those in flight together) go to different members
+    const int owner = t % f.m;
     double2* slot = f.P[owner] + (long long)f.me * f.slot;        // my slot at the owner
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)

@@ -100,3 +100,25 @@ def test_invalid_cond_est():
     for est in (0.5, float("nan")):
         _, res = gpu_qr(X, est)
         assert res["status"] == 1
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("case", ["c1_deg36", "svd_1e12"])
+def test_applied_shift_matches_oracle(complex_, case):
+    """The s of Alg.4 l.5-6 the library added to the Gram diagonal equals the
+    oracle's shift_value(N, n, frobenius_sq(X)) within 1e-13 relative (the device takes
+    ||X||_F^2 as Re tr G, reading #12: same quantity, different summation order)."""
+    if case == "c1_deg36":
+        X, est = filtered_c1(36, complex_)
+        assert est > 1e8
+    else:
+        X, est = ci.svd_synthesized(600, 70, 1e12, 670, complex_), 1e12
+    ref_s = oracle.shift_value(X.shape[0], X.shape[1], oracle.frobenius_sq(X))
+    Q, res = gpu_qr(X, est, complex_)
+    assert res["status"] == 0 and res["variant"] == 3
+    assert abs(res["shift"] - ref_s) <= 1e-13 * ref_s
+    # a non-shifted call reports no shift
+    _, res2 = gpu_qr(X / np.linalg.norm(X), 1e3, complex_)
+    assert res2["variant"] in (2, 3)
+    if res2["variant"] == 2:
+        assert res2["shift"] == 0.0

@@ -81,3 +81,19 @@ def test_hhqr_mode_same_convergence():
         assert np.max(np.abs(res[mode]["lambda"][:nev] - lam[:nev])) <= 1e-9
     assert res[0]["stats"]["iterations"] == res[1]["stats"]["iterations"]
     assert res[0]["stats"]["matvecs"] == res[1]["stats"]["matvecs"]
+
+
+def test_clement_straddles_zero():
+    """Clement spectrum lambda_k = -(N-1) + 2k (straddles 0, so Alg.5 with Lambda = 0 would give
+    rho = 1 in iteration 1): the first QR must not be a single CholeskyQR pass (reading #31 --
+    iteration 1 uses est = u^-1); converges with orthonormal eigenvectors."""
+    N, nev, nex = 1000, 100, 40
+    lam = ci.clement_spectrum(N)
+    A = ci.dense_from_spectrum(lam, 13, True)
+    out, X = run(A, nev, nex, True, tol=1e-10, max_iter=30)
+    assert out["status"] == 0, out
+    assert np.max(np.abs(out["lambda"][:nev] - lam[:nev])) <= 1e-7
+    scale = max(abs(out["stats"]["mu_1"]), abs(out["stats"]["b_sup"]))
+    r = oracle.residuals(A, X[:, :nev], out["lambda"][:nev]) / scale
+    assert np.all(r <= 2e-10)
+    assert np.linalg.norm(X[:, :nev].conj().T @ X[:, :nev] - np.eye(nev)) <= 1e-11

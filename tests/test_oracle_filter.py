@@ -181,3 +181,29 @@ def test_block_cyclic_scheme_equals_global(grid, nb):
     ref, _ = oracle.chebyshev_filter(A, V, degs, b.c, b.e, b.mu_1)
     got = oracle.distributed_filter(A, V, degs, b.c, b.e, b.mu_1, *grid, nb=nb)
     assert relF(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("grid,nb", [((2, 2), 0), ((2, 3), 0), ((3, 2), 4), ((2, 4), 3)])
+@pytest.mark.parametrize("odd", [True, False])
+def test_step_partials_sum_to_global_step(grid, nb, odd):
+    """oracle.step_partial: the partials of a reducing communicator sum to the global step
+    alpha (A - cI) X + beta Y restricted to that communicator's output rows, with beta
+    added by exactly one member and the -cI shift applied exactly once per global row."""
+    p, q = grid
+    N, k = 53, 5
+    rng = np.random.default_rng(7)
+    A = ci.dense_from_spectrum(ci.uniform_spectrum(N), 45, True)
+    X = rng.standard_normal((N, k)) + 1j * rng.standard_normal((N, k))
+    Y = rng.standard_normal((N, k)) + 1j * rng.standard_normal((N, k))
+    alpha, beta, c = 1.7, -0.3, 0.45
+    glob = alpha * (A @ X - c * X) + beta * Y            # A Hermitian: A^H = A
+    owned = oracle.grid._owned
+    for a in range(q if odd else p):                      # one communicator per output block
+        out_rows = owned(N, q, a, nb) if odd else owned(N, p, a, nb)
+        acc = 0
+        for b in range(p if odd else q):
+            i, j = (b, a) if odd else (a, b)
+            in_rows = owned(N, p, i, nb) if odd else owned(N, q, j, nb)
+            acc = acc + oracle.step_partial(A, X[in_rows], Y[out_rows], i, j, p, q, odd,
+                                            alpha, beta, c, b == 0, nb)
+        assert relF(acc, glob[out_rows]) <= 1e-14

@@ -111,6 +111,24 @@ def test_shift_golden(golden):
     assert s == g["s_over_u"] * 2.0 ** -53          # 1.3555823e-12, exact
 
 
+def test_frobenius_sq_complex_golden(golden):
+    """Alg.4 l.5 on complex entries: |3+4i|^2 + |1-2i|^2 = 30 (a real-part-only or
+    unsquared norm gives 10 / 7.24)."""
+    g = golden["frobenius_sq_complex"]
+    X = rows(g["X_re"]) + 1j * rows(g["X_im"])
+    assert oracle.frobenius_sq(X) == g["norm"]
+    assert oracle.frobenius_sq(rows(g["X_re"])) == 10.0          # real X: 9 + 1
+
+
+def test_shift_complex_golden(golden):
+    """The shift the shifted pass adds for the complex golden X: s = 3300 u (Alg.4 l.5-6)."""
+    g, f = golden["shift_complex"], golden["frobenius_sq_complex"]
+    X = rows(f["X_re"]) + 1j * rows(f["X_im"])
+    s = oracle.shift_value(X.shape[0], X.shape[1], oracle.frobenius_sq(X))
+    assert (g["m"], g["n"], g["norm"]) == (X.shape[0], X.shape[1], f["norm"])
+    assert s == g["s_over_u"] * 2.0 ** -53
+
+
 def test_cond_est_golden(golden):
     g = golden["cond_est_t3"]
     c, e = 0.0, 1.0
