@@ -303,26 +303,29 @@ static bool g_fused_attr[2] = {false, false};
 static bool g_dfused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
+// (dynamic shared memory sizes of every variant are set once by preload_kernels)
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
-                                   const CUtensorMap& tX, const ZGemmArgs& a, int grid_tiles = 0) {
+                                   const CUtensorMap& tX, const ZGemmArgs& a, int grid_tiles = 0,
+                                   bool narrow = false) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
+  const int BN = narrow ? ZG_BN_NARROW : ZG_BN;
   const int tiles = a.tail_tiles > 0 ? a.tail_tiles
                     : grid_tiles > 0 ? grid_tiles
-                                     : ((a.N + ZG_BN - 1) / ZG_BN) * ((a.M + ZG_BM - 1) / ZG_BM);
+                                     : ((a.N + BN - 1) / BN) * ((a.M + ZG_BM - 1) / ZG_BM);
   dim3 grid(tiles * (split ? a.k_split : 1));
-  static bool attr[2][2] = {{false, false}, {false, false}};
-  auto go = [&](auto kern, bool& done) -> chase_status_t {
-    if (!done) {
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
-      done = true;
-    }
-    kern<<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  auto go = [&](auto kern, int smem) -> chase_status_t {
+    kern<<<grid, ZG_THREADS, smem, h->stream>>>(tA, tX, a);
     CUDA_TRY(cudaGetLastError());
     return CHASE_OK;
   };
-  if (conj) return split ? go(zgemm_kernel<true, true>, attr[1][1]) : go(zgemm_kernel<true>, attr[1][0]);
-  return split ? go(zgemm_kernel<false, true>, attr[0][1]) : go(zgemm_kernel<false>, attr[0][0]);
+  constexpr int S = ZG_SMEM_BYTES, SN = zg_smem_bytes(ZG_BN_NARROW);
+  if (narrow) {
+    if (conj) return split ? go(zgemm_kernel<true, true, ZG_BN_NARROW>, SN) : go(zgemm_kernel<true, false, ZG_BN_NARROW>, SN);
+    return split ? go(zgemm_kernel<false, true, ZG_BN_NARROW>, SN) : go(zgemm_kernel<false, false, ZG_BN_NARROW>, SN);
+  }
+  if (conj) return split ? go(zgemm_kernel<true, true>, S) : go(zgemm_kernel<true>, S);
+  return split ? go(zgemm_kernel<false, true>, S) : go(zgemm_kernel<false>, S);
 }
 
 static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
@@ -330,25 +333,27 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
                                          const FusedArgs& f, int T);
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
-                                   const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0) {
+                                   const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0,
+                                   bool narrow = false) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
+  const int BN = narrow ? DG_BN_NARROW : DG_BN;
   const int tiles = a.tail_tiles > 0 ? a.tail_tiles
                     : grid_tiles > 0 ? grid_tiles
-                                     : ((a.N + DG_BN - 1) / DG_BN) * ((a.M + DG_BM - 1) / DG_BM);
+                                     : ((a.N + BN - 1) / BN) * ((a.M + DG_BM - 1) / DG_BM);
   dim3 grid(tiles * (split ? a.k_split : 1));
-  static bool attr[2][2] = {{false, false}, {false, false}};
-  auto go = [&](auto kern, bool& done) -> chase_status_t {
-    if (!done) {
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
-      done = true;
-    }
-    kern<<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a);
+  auto go = [&](auto kern, int smem) -> chase_status_t {
+    kern<<<grid, DG_THREADS, smem, h->stream>>>(tA, tX, a);
     CUDA_TRY(cudaGetLastError());
     return CHASE_OK;
   };
-  if (trans) return split ? go(dgemm_kernel<true, true>, attr[1][1]) : go(dgemm_kernel<true>, attr[1][0]);
-  return split ? go(dgemm_kernel<false, true>, attr[0][1]) : go(dgemm_kernel<false>, attr[0][0]);
+  constexpr int S = dg_smem_bytes(DG_BN), SN = dg_smem_bytes(DG_BN_NARROW);
+  if (narrow) {
+    if (trans) return split ? go(dgemm_kernel<true, true, DG_BN_NARROW>, SN) : go(dgemm_kernel<true, false, DG_BN_NARROW>, SN);
+    return split ? go(dgemm_kernel<false, true, DG_BN_NARROW>, SN) : go(dgemm_kernel<false, false, DG_BN_NARROW>, SN);
+  }
+  if (trans) return split ? go(dgemm_kernel<true, true>, S) : go(dgemm_kernel<true>, S);
+  return split ? go(dgemm_kernel<false, true>, S) : go(dgemm_kernel<false>, S);
 }
 
 // One generic GEMM request, dispatched on the handle's dtype.  Pointers are element pointers
@@ -375,6 +380,8 @@ struct GemmReq {
   int64_t split_ld;
   int tail_tiles, tile_offset;  // split-K tail launch (see gemm_tail.cuh)
   int grid_tiles;            // > 0: launch only the first grid_tiles tiles of the raster
+  int narrow;                // the narrow-tile variant (BN = ZG/DG_BN_NARROW); tX has its box
+  const CUtensorMap* tX_narrow;   // run_gemm_tail: X map with the narrow box -> remainder split
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
@@ -393,7 +400,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     a.k_split = r.k_split; a.split_ld = r.split_ld;
     a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles);
+    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0);
   }
   DGemmArgs a;
   a.M = r.M; a.N = r.N; a.K = r.K;
@@ -409,7 +416,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   a.k_split = r.k_split; a.split_ld = r.split_ld;
   a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles);
+  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0);
 }
 
 static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
@@ -447,12 +454,40 @@ static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CU
 // partials, then the fixed-order sum + epilogue.  (T_tail, S) minimise the modelled waves
 // (equal-cost tiles, one CTA per SM); no split when nothing is gained.
 static chase_status_t run_gemm_tail(chase_handle_s* h, const GemmReq& g) {
-  static const bool off = getenv("CHASE_NO_TAIL_SPLIT") != nullptr;   // A/B switch
+  static const bool off = getenv("CHASE_NO_TAIL_SPLIT") != nullptr;   // A/B switches
+  static const bool no_narrow = getenv("CHASE_NO_NARROW") != nullptr;
+  const bool cplx = h->dt == CHASE_C128;
+  if (g.tX_narrow && !no_narrow && !g.narrow && g.M > 0 && g.N > 0 && !g.col_shift && !g.diag_k &&
+      !g.upper_only && g.k_split <= 1) {
+    // ragged width: the N mod BN remainder columns as a narrow-tile GEMM when that pads less
+    const int BNw = cplx ? ZG_BN : DG_BN, BNn = cplx ? ZG_BN_NARROW : DG_BN_NARROW;
+    const int r = g.N % BNw;
+    if (r != 0 && (r + BNn - 1) / BNn * BNn < BNw) {
+      const size_t es = esize_of(h->dt);
+      const int Nmain = g.N - r;
+      if (Nmain > 0) {
+        GemmReq m = g;
+        m.N = Nmain;
+        m.tX_narrow = nullptr;
+        STATUS_TRY(run_gemm_tail(h, m));
+      }
+      GemmReq t = g;
+      t.tX_narrow = nullptr;
+      t.narrow = 1;
+      t.tX = g.tX_narrow;
+      t.N = r;
+      t.x_n0 = g.x_n0 + Nmain;
+      t.out = static_cast<char*>(g.out) + (size_t)Nmain * g.ldo * es;
+      if (g.xin) t.xin = static_cast<const char*>(g.xin) + (size_t)Nmain * g.ldx * es;
+      if (Nmain > 0) h->launches[g.conj ? CAT_HEMM_ODD : CAT_HEMM_EVEN] += 1;
+      return run_gemm_tail(h, t);
+    }
+  }
   if (off || g.M <= 0 || g.N <= 0 || g.col_shift || g.diag_k || g.upper_only || g.abort_flag ||
       g.k_split > 1 || !h->tailws)
     return run_gemm(h, g);
-  const bool cplx = h->dt == CHASE_C128;
-  const int BM = cplx ? ZG_BM : DG_BM, BN = cplx ? ZG_BN : DG_BN, BK = cplx ? ZG_BK : DG_BK;
+  const int BM = cplx ? ZG_BM : DG_BM, BK = cplx ? ZG_BK : DG_BKT;
+  const int BN = cplx ? (g.narrow ? ZG_BN_NARROW : ZG_BN) : (g.narrow ? DG_BN_NARROW : DG_BN);
   const int T = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int SMS = h->num_sms, KT = (g.K + BK - 1) / BK;
   const int full = T / SMS, rem = T % SMS;
@@ -492,12 +527,20 @@ static chase_status_t run_gemm_tail(chase_handle_s* h, const GemmReq& g) {
   STATUS_TRY(run_gemm(h, t));
   TailArgs ta{bS, btail, tmain, g.M, g.N, (long long)g.ldo, (long long)g.ldx, g.alpha, g.beta, g.c,
               g.use_beta, g.band_lo, g.band_hi, g.band_shift, g.band_map};
-  if (cplx)
+  if (cplx && !g.narrow)
     gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M><<<btail, 256, 0, h->stream>>>(
         reinterpret_cast<const double2*>(h->tailws), static_cast<double2*>(g.out),
         static_cast<const double2*>(g.xin), ta);
-  else
+  else if (cplx)
+    gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M><<<btail, 256, 0, h->stream>>>(
+        reinterpret_cast<const double2*>(h->tailws), static_cast<double2*>(g.out),
+        static_cast<const double2*>(g.xin), ta);
+  else if (!g.narrow)
     gemm_tail_epilogue_kernel<double, DG_BM, DG_BN, DG_GROUP_M><<<btail, 256, 0, h->stream>>>(
+        reinterpret_cast<const double*>(h->tailws), static_cast<double*>(g.out),
+        static_cast<const double*>(g.xin), ta);
+  else
+    gemm_tail_epilogue_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M><<<btail, 256, 0, h->stream>>>(
         reinterpret_cast<const double*>(h->tailws), static_cast<double*>(g.out),
         static_cast<const double*>(g.xin), ta);
   CUDA_TRY(cudaGetLastError());
@@ -538,7 +581,7 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
 }
 
 // Tensor maps for the three roles a matrix plays in the GEMM (box shapes of zgemm / dgemm).
-enum MapRole { ROLE_A_NOTRANS, ROLE_A_TRANS, ROLE_X };
+enum MapRole { ROLE_A_NOTRANS, ROLE_A_TRANS, ROLE_X, ROLE_X_NARROW };
 // 3D view of a column-major matrix for the NoTrans A tile: dims {one 128-byte row piece,
 // columns, row pieces} so one TMA box fills the whole BM x BK tile.  Only valid when every
 // column has room for whole 128-byte pieces (ld >= rows rounded up to a piece), since TMA
@@ -574,10 +617,12 @@ static chase_status_t make_role_map(const chase_handle_s* h, CUtensorMap* m, con
     }
   }
   if (h->dt == CHASE_C128) {
-    const int bc = role == ROLE_A_NOTRANS ? 8 : role == ROLE_A_TRANS ? ZG_BM : ZG_BN;
+    const int bc = role == ROLE_A_NOTRANS ? 8 : role == ROLE_A_TRANS ? ZG_BM
+                   : role == ROLE_X_NARROW ? ZG_BN_NARROW : ZG_BN;
     return make_map(m, base, rows, cols, ld, 16, 8, bc);
   }
-  const int bc = role == ROLE_A_NOTRANS ? DG_BK : role == ROLE_A_TRANS ? DG_BM : DG_BN;
+  const int bc = role == ROLE_A_NOTRANS ? DG_BK : role == ROLE_A_TRANS ? DG_BM
+                 : role == ROLE_X_NARROW ? DG_BN_NARROW : DG_BN;
   return make_map(m, base, rows, cols, ld, 8, 16, bc);
 }
 
@@ -679,15 +724,25 @@ static chase_status_t preload_kernels() {
     ok &= smem((const void*)zgemm_kernel<false>, ZG_SMEM_BYTES);
     ok &= smem((const void*)zgemm_kernel<true, true>, ZG_SMEM_BYTES);
     ok &= smem((const void*)zgemm_kernel<false, true>, ZG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_kernel<true>, DG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_kernel<false>, DG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_kernel<true, true>, DG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_kernel<false, true>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<true>, dg_smem_bytes(DG_BN));
+    ok &= smem((const void*)dgemm_kernel<false>, dg_smem_bytes(DG_BN));
+    ok &= smem((const void*)dgemm_kernel<true, true>, dg_smem_bytes(DG_BN));
+    ok &= smem((const void*)dgemm_kernel<false, true>, dg_smem_bytes(DG_BN));
     ok &= smem((const void*)zgemm_fused_kernel<true>, ZG_SMEM_BYTES);
     ok &= smem((const void*)zgemm_fused_kernel<false>, ZG_SMEM_BYTES);
     ok &= smem((const void*)dgemm_fused_kernel<true>, DG_SMEM_BYTES);
     ok &= smem((const void*)dgemm_fused_kernel<false>, DG_SMEM_BYTES);
     ok &= smem((const void*)fused_wait_kernel, 0);
+    ok &= smem((const void*)zgemm_kernel<true, false, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
+    ok &= smem((const void*)zgemm_kernel<false, false, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
+    ok &= smem((const void*)zgemm_kernel<true, true, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
+    ok &= smem((const void*)zgemm_kernel<false, true, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
+    ok &= smem((const void*)dgemm_kernel<true, false, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)dgemm_kernel<false, false, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)dgemm_kernel<true, true, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)dgemm_kernel<false, true, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN, DG_GROUP_M>, 0);
     if (!ok) {
@@ -1111,12 +1166,14 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     CUDA_TRY(cudaMemcpy2DAsync(Cbuf, ldc * es, V, ldv * es, n_r * es, ncols,
                                cudaMemcpyDeviceToDevice, h->stream));
   }
-  CUtensorMap tA_nt, tA_t, tC, tB;
+  CUtensorMap tA_nt, tA_t, tC, tB, tCn, tBn;
   int a3d = 0;
   STATUS_TRY(make_role_map(h, &tA_nt, A_local, n_r, n_c, lda, ROLE_A_NOTRANS, &a3d));
   STATUS_TRY(make_role_map(h, &tA_t, A_local, n_r, n_c, lda, ROLE_A_TRANS));
   STATUS_TRY(make_role_map(h, &tC, Cbuf, n_r, ncols, ldc, ROLE_X));
   STATUS_TRY(make_role_map(h, &tB, Bbuf, n_c, ncols, ldb, ROLE_X));
+  STATUS_TRY(make_role_map(h, &tCn, Cbuf, n_r, ncols, ldc, ROLE_X_NARROW));   // remainder columns
+  STATUS_TRY(make_role_map(h, &tBn, Bbuf, n_c, ncols, ldb, ROLE_X_NARROW));
 
   for (int s = 1; s <= D; ++s) {
     const chase_step_record_t& r = rec[s - 1];
@@ -1138,6 +1195,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.conj = true;
       g.tA = &tA_t;
       g.tX = &tC;
+      g.tX_narrow = &tCn;
       g.M = (int)n_c;
       g.K = (int)n_r;
       g.out = Bbuf + (size_t)r.off * ldb * es;
@@ -1155,6 +1213,7 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       g.tA = &tA_nt;
       g.a3d = a3d;
       g.tX = &tB;
+      g.tX_narrow = &tBn;
       g.M = (int)n_r;
       g.K = (int)n_c;
       g.out = Cbuf + (size_t)r.off * ldc * es;
@@ -1274,14 +1333,15 @@ chase_status_t chase_filter_step(chase_handle_t h, const void* A_local, int64_t 
   const int32_t degs2[1] = {2};
   build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol, h->nb}, 1, degs2, &rec, &mv);
   const chase_step_record_t& r = rec[odd ? 0 : 1];
-  CUtensorMap tA, tX;
+  CUtensorMap tA, tX, tXn;
   int a3d = 0;
   STATUS_TRY(make_role_map(h, &tA, A_local, h->n_r, h->n_c, lda, odd ? ROLE_A_TRANS : ROLE_A_NOTRANS,
                            odd ? nullptr : &a3d));
   STATUS_TRY(make_role_map(h, &tX, X, rows_in, k, ldx, ROLE_X));
+  STATUS_TRY(make_role_map(h, &tXn, X, rows_in, k, ldx, ROLE_X_NARROW));
   GemmReq g{};
   g.conj = odd != 0;
-  g.tA = &tA; g.tX = &tX; g.a3d = a3d;
+  g.tA = &tA; g.tX = &tX; g.tX_narrow = &tXn; g.a3d = a3d;
   g.M = (int)rows_out; g.N = (int)k; g.K = (int)rows_in;
   g.out = Y; g.ldo = ldy;
   g.xin = X; g.ldx = ldx;

@@ -51,6 +51,8 @@ constexpr int ZG_A_BYTES = ZG_A_SLAB * ZG_KS;
 constexpr int ZG_X_BYTES = ZG_X_SLAB * ZG_KS;
 constexpr int ZG_STAGE_BYTES = ZG_A_BYTES + ZG_X_BYTES;
 constexpr int ZG_SMEM_BYTES = ZG_STAGES * ZG_STAGE_BYTES + 1024 + 2 * ZG_STAGES * 8;
+constexpr int ZG_BN_NARROW = 32;  // remainder-column tile width (see zgemm_kernel)
+__host__ __device__ constexpr int zg_smem_bytes(int bn) { return ZG_STAGES * (ZG_A_BYTES + bn * 8 * 16 * ZG_KS) + 1024 + 2 * ZG_STAGES * 8; }
 
 struct ZGemmArgs {
   int M, N, K;
@@ -84,22 +86,26 @@ struct ZGemmArgs {
 };
 
 // SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
-// GEMM with no split arithmetic in its hot loop.
-template <bool CONJ, bool SPLIT = false>
+// GEMM with no split arithmetic in its hot loop.  BN_ (compile time): output columns per CTA --
+// ZG_BN for the bulk of a GEMM, ZG_BN_NARROW for the N mod ZG_BN remainder columns (so a
+// ragged width pads to 32, not 64, columns; the X tensor map box must match).
+template <bool CONJ, bool SPLIT = false, int BN_ = ZG_BN>
 __global__ void __launch_bounds__(ZG_THREADS, 1)
     zgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const ZGemmArgs g) {
+  constexpr int WN_ = BN_ / ZG_WNW, NT_ = WN_ / 8;               // warp tile columns, n8 tiles
+  constexpr int XS_ = BN_ * 8 * 16, XB_ = XS_ * ZG_KS, SB_ = ZG_A_BYTES + XB_;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128B swizzle, derived from the __shared__ array so every
   // fragment load stays an LDS (a pointer rebuilt from an integer becomes a generic LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * SB_);
   uint64_t* empty = full + ZG_STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grouped rasterisation (1D grid): consecutive CTAs walk ZG_GROUP_M m-tiles, then the next
   // n-tile, so the CTAs resident at one time share A rows and X columns in L2
-  const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
+  const int n_tiles = (g.N + BN_ - 1) / BN_, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   // split-K: the grid holds k_split copies of the tile grid, copy s sums its own k range
   const int tiles_launch = SPLIT && g.tail_tiles > 0 ? g.tail_tiles : n_tiles * m_tiles;
   const int split = SPLIT ? (int)blockIdx.x / tiles_launch : 0;
@@ -109,8 +115,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int first_m = group * ZG_GROUP_M;
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
   const int within = bid - group * ZG_GROUP_M * n_tiles;
-  const int m0 = (first_m + within % gm) * ZG_BM, n0 = (within / gm) * ZG_BN;
-  if (g.upper_only && m0 > n0 + ZG_BN - 1) return;
+  const int m0 = (first_m + within % gm) * ZG_BM, n0 = (within / gm) * BN_;
+  if (g.upper_only && m0 > n0 + BN_ - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
   const int KT_all = (g.K + ZG_BK - 1) / ZG_BK;
   const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
@@ -130,8 +136,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   // stage `s` <- k-tile `kt` (TMA, completion on full[s]); issued by thread 0 only
   auto issue = [&](int kt, int s) {
-    mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
-    uint8_t* sa = smem + s * ZG_STAGE_BYTES;
+    mbar_arrive_expect_tx(&full[s], SB_);
+    uint8_t* sa = smem + s * SB_;
     uint8_t* sx = sa + ZG_A_BYTES;
 #pragma unroll
     for (int u = 0; u < ZG_KS; ++u) {
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
             tma_load_2d(sau + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
         }
       }
-      tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
+      tma_load_2d(sx + u * XS_, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
   };
 #if ZG_WS
@@ -181,11 +187,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // -------------------------------------------------------------- consumer warps
   const int wm = cwarp & 3, wn = cwarp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  double acc_re[2][ZG_NT][4], acc_im[2][ZG_NT][4];
+  double acc_re[2][NT_][4], acc_im[2][NT_][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < ZG_NT; ++j)
+    for (int j = 0; j < NT_; ++j)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
 
@@ -193,13 +199,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // sub-step of the next k-tile, after its full barrier) are issued before the DMMAs of t.
   constexpr int SUBS = 2 * ZG_KS;                      // m16n8k4 sub-steps per k-tile
   struct Frag {
-    double2 a[2][2], b[ZG_NT];
+    double2 a[2][2], b[NT_];
   };
   auto load = [&](Frag& f, int kt, int sub) {
     const int u = sub >> 1, h = sub & 1;
     const int k = 2 * tq + h;                          // k inside the 8-wide slab u
-    const uint8_t* sa = smem + (kt % ZG_STAGES) * ZG_STAGE_BYTES + u * ZG_A_SLAB;
-    const uint8_t* sx = smem + (kt % ZG_STAGES) * ZG_STAGE_BYTES + ZG_A_BYTES + u * ZG_X_SLAB;
+    const uint8_t* sa = smem + (kt % ZG_STAGES) * SB_ + u * ZG_A_SLAB;
+    const uint8_t* sx = smem + (kt % ZG_STAGES) * SB_ + ZG_A_BYTES + u * XS_;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -210,15 +216,15 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         f.a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
       }
 #pragma unroll
-    for (int nt = 0; nt < ZG_NT; ++nt) {
-      const int n = wn * ZG_WN + nt * 8 + gq;
+    for (int nt = 0; nt < NT_; ++nt) {
+      const int n = wn * WN_ + nt * 8 + gq;
       f.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
     }
     if (kt * ZG_BK + 8 * u + k >= Krem) {               // K tail (the TMA box may hold stale data)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) f.a[mt][0] = f.a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) f.b[nt] = make_double2(0.0, 0.0);
+      for (int nt = 0; nt < NT_; ++nt) f.b[nt] = make_double2(0.0, 0.0);
     }
   };
   auto mma = [&](const Frag& f) {
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) {
+      for (int nt = 0; nt < NT_; ++nt) {
         dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].x);
         dmma_16x8x4(acc_im[mt][nt], f.a[mt][0].x, f.a[mt][1].x, f.b[nt].y);
       }
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) {
+      for (int nt = 0; nt < NT_; ++nt) {
         const double bre = CONJ ? f.b[nt].y : -f.b[nt].y;
         const double bim = CONJ ? -f.b[nt].x : f.b[nt].x;
         dmma_16x8x4(acc_re[mt][nt], f.a[mt][0].y, f.a[mt][1].y, bre);
@@ -276,11 +282,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < ZG_NT; ++nt)
+    for (int nt = 0; nt < NT_; ++nt)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
-        const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
+        const int col = n0 + wn * WN_ + nt * 8 + 2 * tq + (r & 1);
         if (row < g.M && col < g.N) {
           double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
           const int bsrc = g.band_map != nullptr ? g.band_map[row]
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           vr *= g.alpha;
           vi *= g.alpha;
           double2* o = SPLIT && g.tail_tiles > 0
-                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (ZG_BM * ZG_BN) +
+                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (ZG_BM * BN_) +
                                  (row - m0) + (long long)(col - n0) * ZG_BM
                            : g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) {
