@@ -135,6 +135,7 @@ struct chase_handle_s {
   void* Gws = nullptr;      // n_max x n_max (Gram / R)
   void* Wws = nullptr;      // n_r x n_max (TRSM output)
   void* Rinv = nullptr;     // 64 x n_max (inverted diagonal blocks of R)
+  char* Rfws = nullptr;     // R^{-1} n_max x n_max, then the recursive-doubling temp
   void* B2ws = nullptr;     // n_c x n_max (C redistributed into B-layout, Alg.2 l.23)
   char* eigws = nullptr;    // Jacobi eigensolver region (see eig_bytes)
   char* c2ws = nullptr;     // solver: C2
@@ -216,7 +217,7 @@ static size_t esize_of(chase_dtype_t dt) { return dt == CHASE_C128 ? 16 : 8; }
 
 constexpr int TAIL_TILES_MAX = 320;   // split-K tail: tiles x copies held (128 KB each)
 struct WsLayout {
-  size_t b, g, w, rinv, b2, ritz, nrm, maps, eig, c2, lan, hh, tail, info, s, total;
+  size_t b, g, w, rinv, rf, b2, ritz, nrm, maps, eig, c2, lan, hh, tail, info, s, total;
 };
 constexpr int LANCZOS_K = 25;       // Lanczos steps per run (bounds, Alg.1 l.2)
 constexpr int LANCZOS_RUNS = 4;     // independent runs pooled for the DoS estimate
@@ -271,6 +272,8 @@ static WsLayout ws_layout(const chase_handle_s* h) {
   off += align256((size_t)(std::max(h->n_r, h->n_c) + 2) * h->n_max * es);
   L.rinv = off;
   off += align256((size_t)TRTRI_NB * (h->n_max + TRTRI_NB) * es);
+  L.rf = off;                                           // R^{-1} (n_max^2) + doubling temp
+  off += 2 * align256((size_t)pad_ld(h->n_max) * h->n_max * es);
   L.b2 = off;                                           // residual: C redistributed to B-layout
   off += align256((size_t)pad_ld(h->n_c) * h->n_max * es);
   L.ritz = off;
@@ -306,14 +309,14 @@ static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B swi
 // (dynamic shared memory sizes of every variant are set once by preload_kernels)
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a, int grid_tiles = 0,
-                                   bool narrow = false) {
+                                   bool narrow = false, int nbatch = 1) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
   const int BN = narrow ? ZG_BN_NARROW : ZG_BN;
   const int tiles = a.tail_tiles > 0 ? a.tail_tiles
                     : grid_tiles > 0 ? grid_tiles
                                      : ((a.N + BN - 1) / BN) * ((a.M + ZG_BM - 1) / ZG_BM);
-  dim3 grid(tiles * (split ? a.k_split : 1));
+  dim3 grid(tiles * (split ? a.k_split : 1), std::max(1, nbatch));
   auto go = [&](auto kern, int smem) -> chase_status_t {
     kern<<<grid, ZG_THREADS, smem, h->stream>>>(tA, tX, a);
     CUDA_TRY(cudaGetLastError());
@@ -334,14 +337,14 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0,
-                                   bool narrow = false) {
+                                   bool narrow = false, int nbatch = 1) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
   const int BN = narrow ? DG_BN_NARROW : DG_BN;
   const int tiles = a.tail_tiles > 0 ? a.tail_tiles
                     : grid_tiles > 0 ? grid_tiles
                                      : ((a.N + BN - 1) / BN) * ((a.M + DG_BM - 1) / DG_BM);
-  dim3 grid(tiles * (split ? a.k_split : 1));
+  dim3 grid(tiles * (split ? a.k_split : 1), std::max(1, nbatch));
   auto go = [&](auto kern, int smem) -> chase_status_t {
     kern<<<grid, DG_THREADS, smem, h->stream>>>(tA, tX, a);
     CUDA_TRY(cudaGetLastError());
@@ -382,11 +385,17 @@ struct GemmReq {
   int grid_tiles;            // > 0: launch only the first grid_tiles tiles of the raster
   int narrow;                // the narrow-tile variant (BN = ZG/DG_BN_NARROW); tX has its box
   const CUtensorMap* tX_narrow;   // run_gemm_tail: X map with the narrow box -> remainder split
+  int tri_k;                 // X upper triangular: per-tile K = min(K, n0 + BN) (TRSM by R^{-1})
+  int nbatch;                // > 1: batched launch (gridDim.y), strides bat_a / bat_x / bat_out
+  int bat_a, bat_x;
+  int64_t bat_out;
 };
 
 static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   if (h->dt == CHASE_C128) {
-    ZGemmArgs a;
+    ZGemmArgs a{};
+    a.tri_k = r.tri_k;
+    a.bat_a = r.bat_a; a.bat_x = r.bat_x; a.bat_out = r.bat_out;
     a.M = r.M; a.N = r.N; a.K = r.K;
     a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
     a.out = static_cast<double2*>(r.out); a.ldo = r.ldo;
@@ -400,9 +409,11 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     a.k_split = r.k_split; a.split_ld = r.split_ld;
     a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0);
+    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch);
   }
-  DGemmArgs a;
+  DGemmArgs a{};
+  a.tri_k = r.tri_k;
+  a.bat_a = r.bat_a; a.bat_x = r.bat_x; a.bat_out = r.bat_out;
   a.M = r.M; a.N = r.N; a.K = r.K;
   a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
   a.out = static_cast<double*>(r.out); a.ldo = r.ldo;
@@ -416,7 +427,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   a.k_split = r.k_split; a.split_ld = r.split_ld;
   a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0);
+  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch);
 }
 
 static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
@@ -991,6 +1002,7 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes) {
   h->Gws = base + L.g;
   h->Wws = base + L.w;
   h->Rinv = base + L.rinv;
+  h->Rfws = base + L.rf;
   h->B2ws = base + L.b2;
   h->eigws = base + L.eig;
   h->c2ws = base + L.c2;
@@ -1373,8 +1385,36 @@ void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n
 
 struct QrMaps {
   CUtensorMap vA_t, vA_nt, vX, gA_t, gX, wA_nt, rinvX;
+  CUtensorMap gA_nt, rfA_nt, rfX, tmpX;      // TRSM through R^{-1} (recursive doubling)
   int v_a3d = 0, w_a3d = 0;
 };
+
+// Split-K factor of the Gram GEMM: the upper-triangle tiles of an n x n output are few (C2:
+// ~600 tiles = 4.05 waves on 148 SMs); S K-slices of them fill the waves.  S minimises the
+// modelled waves (in units of a full-K tile), with K/S >= 1024 and the S partial n x n matrices
+// fitting in the W workspace.
+static int gram_split(const chase_handle_s* h, int n, int64_t K) {
+  static const bool off = getenv("CHASE_NO_GRAM_SPLIT") != nullptr;   // A/B switch
+  if (off) return 1;
+  const bool cplx = h->dt == CHASE_C128;
+  const int BM = cplx ? ZG_BM : DG_BM, BN = cplx ? ZG_BN : DG_BN;
+  const int n_tiles = (n + BN - 1) / BN, m_tiles = (n + BM - 1) / BM;
+  int64_t up = 0;
+  for (int j = 0; j < n_tiles; ++j) up += std::min<int64_t>(m_tiles, (int64_t)(j * BN + BN - 1) / BM + 1);
+  const int64_t wcap = (std::max(h->n_r, h->n_c) + 2) * h->n_max;           // W elements
+  const int64_t mat = pad_ld(n) * (int64_t)n;
+  int best = 1;
+  double best_w = (double)((up + h->num_sms - 1) / h->num_sms);
+  for (int S = 2; S <= 8; ++S) {
+    if (K / S < 1024 || S * mat > wcap) break;
+    const double w = (double)((up * S + h->num_sms - 1) / h->num_sms) / S;
+    if (w < best_w - 0.02) {
+      best_w = w;
+      best = S;
+    }
+  }
+  return best;
+}
 
 // One Gram/POTRF/TRSM round; returns CHASE_ECHOL with *info set when POTRF fails (V untouched).
 chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool shifted,
@@ -1384,16 +1424,31 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
   char* G = static_cast<char*>(h->Gws);
   char* Vc = static_cast<char*>(V);
   const int64_t ldg = pad_ld(n);
-  // Gram G = V^H V (upper tiles), Alg.3 l.3
+  // Gram G = V^H V (upper tiles), Alg.3 l.3; split over K into partials in W when that fills
+  // the waves better, then summed in fixed order (deterministic)
   {
+    const int S = gram_split(h, n, n_r);
     GemmReq g{};
     g.conj = true; g.tA = &mp.vA_t; g.tX = &mp.vX;
     g.M = n; g.N = n; g.K = (int)n_r;
-    g.out = G; g.ldo = ldg; g.xin = nullptr; g.ldx = 0;
+    g.out = S > 1 ? h->Wws : G; g.ldo = ldg; g.xin = nullptr; g.ldx = 0;
     g.alpha = 1.0; g.beta = 0.0; g.c = 0.0; g.use_beta = 0;
     g.band_lo = g.band_hi = 0; g.band_shift = 0; g.upper_only = 1; g.abort_flag = nullptr;
-    ProfScope ps(h, CAT_GRAM, 1);
+    g.k_split = S; g.split_ld = (int64_t)ldg * n;
+    ProfScope ps(h, CAT_GRAM, S > 1 ? 2 : 1);
     STATUS_TRY(run_gemm(h, g));
+    if (S > 1) {
+      const dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
+      if (h->dt == CHASE_C128)
+        hh_splitsum_kernel<double2><<<grid, 256, 0, h->stream>>>(
+            static_cast<const double2*>(h->Wws), (long long)ldg * n, S, n, (int)ldg,
+            reinterpret_cast<double2*>(G), (int)ldg);
+      else
+        hh_splitsum_kernel<double><<<grid, 256, 0, h->stream>>>(
+            static_cast<const double*>(h->Wws), (long long)ldg * n, S, n, (int)ldg,
+            reinterpret_cast<double*>(G), (int)ldg);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
   // Alg.3 l.4 AllReduce over the column communicator
   if (h->p > 1) STATUS_TRY(allreduce(h, G, (size_t)ldg * n, h->ccomm));
@@ -1438,7 +1493,70 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
   *info = *h->h_info;
   if (shifted) h->last_shift = *h->h_shift;
   if (*info != 0) return CHASE_ECHOL;
-  // TRSM V <- V R^{-1}, Alg.3 l.6: right-looking blocked with inverted 64x64 diagonal blocks.
+  // TRSM V <- V R^{-1}, Alg.3 l.6, as R^{-1} by recursive doubling + ONE GEMM:
+  //   64x64 diagonal blocks inverted in smem (trtri_diag_kernel); then for b = 64, 128, ...:
+  //   each pair of inverted b-blocks becomes a 2b-block, X12 = -R11^{-1} (R12 R22^{-1});
+  //   W = V R^{-1} on the tensor cores with a triangular K range per output tile (tri_k, longest
+  //   tiles first); W copied back into V.  The products X R^{-1} differ from a triangular solve
+  //   by O(u kappa(R)^2) inside span(X) and O(u kappa(R)) across it -- within CholeskyQR's own
+  //   u kappa^2 (Gram) loss, which the next pass removes (TRSM).
+  static const bool blocked_trsm = getenv("CHASE_TRSM_BLOCKED") != nullptr;   // A/B switch
+  if (!blocked_trsm) {
+    ProfScope ps(h, CAT_TRSM, 0);
+    const int64_t ldf = pad_ld(n), ldw = pad_ld(n_r);
+    char* Rf = h->Rfws;
+    char* Tmp = h->Rfws + align256((size_t)pad_ld(h->n_max) * h->n_max * es);
+    char* W = static_cast<char*>(h->Wws);
+    const int nblk = (n + TRTRI_NB - 1) / TRTRI_NB;
+    CUDA_TRY(cudaMemsetAsync(Rf, 0, (size_t)ldf * n * es, h->stream));
+    if (h->dt == CHASE_C128)
+      trtri_diag_kernel<double2><<<nblk, TRTRI_NB, trtri_smem<double2>(), h->stream>>>(
+          reinterpret_cast<const double2*>(G), ldg, n, reinterpret_cast<double2*>(Rf), ldf, 1);
+    else
+      trtri_diag_kernel<double><<<nblk, TRTRI_NB, trtri_smem<double>(), h->stream>>>(
+          reinterpret_cast<const double*>(G), ldg, n, reinterpret_cast<double*>(Rf), ldf, 1);
+    CUDA_TRY(cudaGetLastError());
+    h->launches[CAT_TRSM]++;
+    // level b: pairs p = 0..np-1 at i0 = 2 b p (block-diagonal, independent): the full pairs in
+    // one batched launch per product, a trailing short pair (b2 < b) in its own
+    for (int b = TRTRI_NB; b < n; b *= 2) {
+      const int npairs = (n - b + 2 * b - 1) / (2 * b);       // pairs with i0 + b < n
+      const int nfull = (n / (2 * b));                          // pairs with b2 == b
+      for (int part = 0; part < 2; ++part) {
+        const int p0 = part == 0 ? 0 : nfull, cnt = part == 0 ? nfull : npairs - nfull;
+        if (cnt <= 0) continue;
+        const int i0 = 2 * b * p0, j0 = i0 + b, b2 = std::min(i0 + 2 * b, n) - j0;
+        const int st = 2 * b;
+        GemmReq g{};                          // Tmp[i0:j0, j0:j0+b2] = R[i0:j0, j0:j0+b2] R22^{-1}
+        g.conj = false; g.tA = &mp.gA_nt; g.tX = &mp.rfX;
+        g.M = b; g.N = b2; g.K = b2;
+        g.a_d0 = i0; g.a_d1 = j0; g.x_k0 = j0; g.x_n0 = j0;
+        g.out = Tmp + ((size_t)i0 + (size_t)j0 * ldf) * es; g.ldo = ldf; g.alpha = 1.0;
+        g.nbatch = cnt; g.bat_a = st; g.bat_x = st; g.bat_out = (int64_t)st * (1 + ldf);
+        STATUS_TRY(run_gemm(h, g));
+        GemmReq g2{};                         // X12 = -R11^{-1} Tmp
+        g2.conj = false; g2.tA = &mp.rfA_nt; g2.tX = &mp.tmpX;
+        g2.M = b; g2.N = b2; g2.K = b;
+        g2.a_d0 = i0; g2.a_d1 = i0; g2.x_k0 = i0; g2.x_n0 = j0;
+        g2.out = Rf + ((size_t)i0 + (size_t)j0 * ldf) * es; g2.ldo = ldf; g2.alpha = -1.0;
+        g2.nbatch = cnt; g2.bat_a = st; g2.bat_x = st; g2.bat_out = (int64_t)st * (1 + ldf);
+        STATUS_TRY(run_gemm(h, g2));
+        h->launches[CAT_TRSM] += 2;
+      }
+    }
+    {
+      GemmReq g{};                            // W = V R^{-1}
+      g.conj = false; g.tA = &mp.vA_nt; g.tX = &mp.rfX; g.a3d = mp.v_a3d;
+      g.M = (int)n_r; g.N = n; g.K = n; g.tri_k = 1;
+      g.out = W; g.ldo = ldw; g.alpha = 1.0;
+      STATUS_TRY(run_gemm(h, g));
+      h->launches[CAT_TRSM]++;
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(Vc, ldv * es, W, ldw * es, n_r * es, n, cudaMemcpyDeviceToDevice,
+                               h->stream));
+    return CHASE_OK;
+  }
+  // blocked variant (CHASE_TRSM_BLOCKED): right-looking with inverted 64x64 diagonal blocks.
   // Solved block columns go to W (W_k = V_k Rinv_kk), the trailing columns of V are updated
   // with V_rest -= W_k R[k, rest]; W is copied back into V at the end.
   {
@@ -1533,6 +1651,14 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   STATUS_TRY(make_role_map(h, &mp.gX, h->Gws, n, n, pad_ld(n), ROLE_X));
   STATUS_TRY(make_role_map(h, &mp.wA_nt, h->Wws, h->n_r, n, pad_ld(h->n_r), ROLE_A_NOTRANS, &mp.w_a3d));
   STATUS_TRY(make_role_map(h, &mp.rinvX, h->Rinv, TRTRI_NB, n, TRTRI_NB, ROLE_X));
+  {
+    char* Rf = h->Rfws;
+    char* Tmp = h->Rfws + align256((size_t)pad_ld(h->n_max) * h->n_max * esize_of(h->dt));
+    STATUS_TRY(make_role_map(h, &mp.gA_nt, h->Gws, n, n, pad_ld(n), ROLE_A_NOTRANS));
+    STATUS_TRY(make_role_map(h, &mp.rfA_nt, Rf, n, n, pad_ld(n), ROLE_A_NOTRANS));
+    STATUS_TRY(make_role_map(h, &mp.rfX, Rf, n, n, pad_ld(n), ROLE_X));
+    STATUS_TRY(make_role_map(h, &mp.tmpX, Tmp, n, n, pad_ld(n), ROLE_X));
+  }
 
   // Alg.4: est > 1e8 -> shifted CholeskyQR2; est < 20 -> CholeskyQR; else CholeskyQR2
   int variant = cond_est > 1e8 ? CHASE_QR_SHIFTED : (cond_est < 20.0 ? CHASE_QR_CHOL1 : CHASE_QR_CHOL2);

@@ -77,6 +77,9 @@ struct DGemmArgs {
   long long split_ld;
   int tail_tiles;          // split-K tail of a big GEMM: see zgemm.cuh
   int tile_offset;
+  int tri_k;               // X upper triangular: see zgemm.cuh
+  int bat_a, bat_x;        // batched launch: see zgemm.cuh
+  long long bat_out;
 };
 
 __device__ __forceinline__ int dg_kperm(int t, int h) {
@@ -115,14 +118,20 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   const int first_m = group * DG_GROUP_M;
   const int gm = min(DG_GROUP_M, m_tiles - first_m);
   const int within = bid - group * DG_GROUP_M * n_tiles;
-  const int m0 = (first_m + within % gm) * DG_BM, n0 = (within / gm) * BN_;
+  const int m0 = (first_m + within % gm) * DG_BM;
+  const int n0 = (g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
   if (g.upper_only && m0 > n0 + BN_ - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int KT_all = (g.K + DG_BKT - 1) / DG_BKT;
+  const int Kt = g.tri_k ? min(g.K, n0 + BN_) : g.K;      // K of this tile
+  const int KT_all = (Kt + DG_BKT - 1) / DG_BKT;
   const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * DG_BKT;
-  const int Krem = g.K - kbase;                    // K left from this split's first k
+  const int Krem = Kt - kbase;                     // K left from this split's first k
+  const int bz = blockIdx.y;                       // batch index (0 unless batched)
+  const int a_d0 = g.a_d0 + bz * g.bat_a, a_d1 = g.a_d1 + bz * g.bat_a;
+  const int x_k0 = g.x_k0 + bz * g.bat_x, x_n0 = g.x_n0 + bz * g.bat_x;
+  double* const gout = g.out + bz * g.bat_out;
   const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
@@ -143,17 +152,17 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       uint8_t* sx = smem + s * SB_ + AB_ + u * SLX;
       const int k0 = kt * DG_BKT + u * DG_BK + dk;
       if (TRANS) {
-        tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);     // box 16 k x 128 m
+        tma_load_2d(sa, &tmA, a_d0 + k0, a_d1 + m0, &full[s]);     // box 16 k x 128 m
       } else {
         if (g.a3d) {
-          tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 16, &full[s]);
+          tma_load_3d(sa, &tmA, 0, a_d1 + k0, (a_d0 + m0) / 16, &full[s]);
         } else {
 #pragma unroll
           for (int b = 0; b < DG_BM / 16; ++b)                    // box 16 m x 16 k
-            tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+            tma_load_2d(sa + b * 2048, &tmA, a_d0 + m0 + 16 * b, a_d1 + k0, &full[s]);
         }
       }
-      tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);       // box 16 k x BN n
+      tma_load_2d(sx, &tmX, x_k0 + k0, x_n0 + n0, &full[s]);       // box 16 k x BN n
     }
   };
   if (threadIdx.x == 0) {
@@ -252,9 +261,9 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
           if (g.col_shift != nullptr) v -= g.col_shift[col] * g.y2[(long long)row + (long long)col * g.ldy2];
           v *= g.alpha;
           double* o = SPLIT && g.tail_tiles > 0
-                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (DG_BM * BN_) +
+                           ? gout + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (DG_BM * BN_) +
                                  (row - m0) + (long long)(col - n0) * DG_BM
-                           : g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
+                           : gout + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) v += g.beta * *o;
           *o = v;
         }

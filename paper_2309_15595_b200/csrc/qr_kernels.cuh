@@ -135,9 +135,11 @@ __global__ void __launch_bounds__(PANEL_BLOCK)
   }
 }
 
-// Inverses of the diagonal blocks of the upper-triangular R (blocked TRSM with inverted
-// diagonal blocks): CTA b inverts R[kb:kb+nb, kb:kb+nb], kb = 64 b, into Rinv[0:64, kb:kb+64]
-// (column-major, ld 64, zeros below the diagonal and in the padding of a short last block).
+// Inverses of the diagonal blocks of the upper-triangular R: CTA b inverts
+// R[kb:kb+nb, kb:kb+nb], kb = 64 b, into Rinv[0:64, kb:kb+64] (full == 0: compact, ld 64, zeros
+// below the diagonal and in the padding of a short last block) or into the diagonal block
+// Rinv[kb:kb+nb, kb:kb+nb] of an n x n matrix with leading dimension ldr (full == 1, the seed of
+// the recursive-doubling inverse of R; nothing outside the block is written).
 // Thread j solves R_kk x = e_j by back substitution:
 //   x_j = 1 / R_jj,  x_i = -(sum_{l=i+1..j} R_il x_l) / R_ii   (i = j-1 .. 0).
 constexpr int TRTRI_NB = 64;
@@ -145,7 +147,7 @@ template <typename T>
 constexpr int trtri_smem() { return 2 * TRTRI_NB * TRTRI_NB * (int)sizeof(T); }
 template <typename T>
 __global__ void __launch_bounds__(TRTRI_NB)
-    trtri_diag_kernel(const T* G, long long ld, int n, T* Rinv) {
+    trtri_diag_kernel(const T* G, long long ld, int n, T* Rinv, long long ldr = TRTRI_NB, int full = 0) {
   extern __shared__ __align__(16) unsigned char qr_dyn[];
   T (*R)[TRTRI_NB] = reinterpret_cast<T (*)[TRTRI_NB]>(qr_dyn);                 // R[i][l]
   T (*X)[TRTRI_NB] = reinterpret_cast<T (*)[TRTRI_NB]>(qr_dyn + TRTRI_NB * TRTRI_NB * sizeof(T));
@@ -172,7 +174,12 @@ __global__ void __launch_bounds__(TRTRI_NB)
       X[i][j] = s_div(s_add(a0, a1), s_re(R[i][i]));
     }
   }
-  for (int i = 0; i < TRTRI_NB; ++i) Rinv[(long long)i + (long long)(kb + j) * TRTRI_NB] = X[i][j];
+  if (full) {
+    if (j < nb)
+      for (int i = 0; i < nb; ++i) Rinv[(long long)(kb + i) + (long long)(kb + j) * ldr] = X[i][j];
+  } else {
+    for (int i = 0; i < TRTRI_NB; ++i) Rinv[(long long)i + (long long)(kb + j) * ldr] = X[i][j];
+  }
 }
 
 // Residual norms, Alg.2 l.26 "nrm <- SquaredNorm(B)": nrm[c] = sum_r |B[r, c]|^2 over the local

@@ -83,6 +83,11 @@ struct ZGemmArgs {
   int tile_offset;         //   of the raster (the wave-quantisation tail of a big GEMM), and each
                            //   partial tile is stored tile-local: out + (s tail_tiles + j) BM BN,
                            //   column-major with ld BM (gemm_tail_epilogue_kernel finishes them)
+  int tri_k;               // X upper triangular (V R^{-1} of the TRSM): tile (m0, n0) sums only
+                           //   k < min(K, n0 + BN); n-tiles rastered last-first (longest first)
+  int bat_a, bat_x;        // batched launch (gridDim.y > 1, block-diagonal sub-problems of the
+  long long bat_out;       //   recursive-doubling TRTRI): batch z adds z*bat_a to both A map
+                           //   coordinates, z*bat_x to both X map coordinates, z*bat_out to out
 };
 
 // SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
@@ -115,14 +120,20 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int first_m = group * ZG_GROUP_M;
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
   const int within = bid - group * ZG_GROUP_M * n_tiles;
-  const int m0 = (first_m + within % gm) * ZG_BM, n0 = (within / gm) * BN_;
+  const int m0 = (first_m + within % gm) * ZG_BM;
+  const int n0 = (g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
   if (g.upper_only && m0 > n0 + BN_ - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int KT_all = (g.K + ZG_BK - 1) / ZG_BK;
+  const int Kt = g.tri_k ? min(g.K, n0 + BN_) : g.K;      // K of this tile
+  const int KT_all = (Kt + ZG_BK - 1) / ZG_BK;
   const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * ZG_BK;
-  const int Krem = g.K - kbase;                    // K left from this split's first k
+  const int Krem = Kt - kbase;                     // K left from this split's first k
+  const int bz = blockIdx.y;                       // batch index (0 unless batched)
+  const int a_d0 = g.a_d0 + bz * g.bat_a, a_d1 = g.a_d1 + bz * g.bat_a;
+  const int x_k0 = g.x_k0 + bz * g.bat_x, x_n0 = g.x_n0 + bz * g.bat_x;
+  double2* const gout = g.out + bz * g.bat_out;
   const int dk = (g.diag_k == 1 ? n0 : (g.diag_k == 2 ? m0 : 0)) + kbase;   // per-CTA k offset
 
   if (threadIdx.x == 0) {
@@ -145,18 +156,18 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       uint8_t* sau = sa + u * ZG_A_SLAB;
       if (CONJ) {
         // opA[m][k] = conj(A[k][m]); A rows (k) contiguous: one 128 x 8 box, row = m
-        tma_load_2d(sau, &tmA, 2 * (g.a_d0 + k0), g.a_d1 + m0, &full[s]);
+        tma_load_2d(sau, &tmA, 2 * (a_d0 + k0), a_d1 + m0, &full[s]);
       } else {
         // A rows (m) contiguous: 16 boxes of 8 m x 8 k, box b holds rows [8b, 8b+8), row = k
         if (g.a3d) {
-          tma_load_3d(sau, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 8, &full[s]);
+          tma_load_3d(sau, &tmA, 0, a_d1 + k0, (a_d0 + m0) / 8, &full[s]);
         } else {
 #pragma unroll
           for (int b = 0; b < ZG_BM / 8; ++b)
-            tma_load_2d(sau + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
+            tma_load_2d(sau + b * 1024, &tmA, 2 * (a_d0 + m0 + 8 * b), a_d1 + k0, &full[s]);
         }
       }
-      tma_load_2d(sx + u * XS_, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
+      tma_load_2d(sx + u * XS_, &tmX, 2 * (x_k0 + k0), x_n0 + n0, &full[s]);
     }
   };
 #if ZG_WS
@@ -305,9 +316,9 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
           vr *= g.alpha;
           vi *= g.alpha;
           double2* o = SPLIT && g.tail_tiles > 0
-                           ? g.out + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (ZG_BM * BN_) +
+                           ? gout + ((long long)split * g.tail_tiles + (long long)(bid - g.tile_offset)) * (ZG_BM * BN_) +
                                  (row - m0) + (long long)(col - n0) * ZG_BM
-                           : g.out + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
+                           : gout + (long long)split * g.split_ld + (long long)row + (long long)col * g.ldo;
           if (g.use_beta) {
             const double2 old = *o;
             vr += g.beta * old.x;
