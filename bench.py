@@ -165,44 +165,56 @@ class Clocks:
 
 
 class NvLink:
-    """NVLink data bytes moved by this GPU (NVML THROUGHPUT_DATA counters, KiB, summed over the
-    links) -- the fused kernel's peer traffic, read around the timed region."""
+    """NVLink data bytes moved by this GPU, summed over its active links, read around the timed
+    region (the fused kernel's peer traffic).  NVML field values: COUNT_XMIT/RCV_BYTES (bytes;
+    the Blackwell counters), else THROUGHPUT_DATA_TX/RX (KiB)."""
 
     def __init__(self, index: int):
-        self.h = None
+        self.h, self.err, self.links = None, None, []
         try:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.links = [l for l in range(18)
-                          if self._safe(lambda: pynvml.nvmlDeviceGetNvLinkState(self.h, l)) == 1]
-        except Exception:
-            self.h = None
-
-    @staticmethod
-    def _safe(f):
-        try:
-            return f()
-        except Exception:
-            return None
+            for l in range(18):
+                try:
+                    if pynvml.nvmlDeviceGetNvLinkState(self.h, l) == 1:
+                        self.links.append(l)
+                except Exception:
+                    pass
+            if not self.links:
+                self.err = "no active NVLink reported by NVML"
+        except Exception as exc:
+            self.h, self.err = None, f"NVML: {exc}"
 
     def read(self):
         if self.h is None or not self.links:
             return None
         nv = self.nv
-        try:
-            tx = rx = 0
-            for l in self.links:
-                vals = nv.nvmlDeviceGetFieldValues(self.h, [(nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, l),
-                                                            (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, l)])
-                if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
-                    return None
-                tx += vals[0].value.ullVal
-                rx += vals[1].value.ullVal
-            return 1024 * tx, 1024 * rx
-        except Exception:
-            return None
+        for tx_id, rx_id, scale, name in (
+                (getattr(nv, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", None),
+                 getattr(nv, "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", None), 1, "COUNT_XMIT/RCV_BYTES"),
+                (nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024,
+                 "THROUGHPUT_DATA_TX/RX")):
+            if tx_id is None:
+                continue
+            try:
+                tx = rx = 0
+                ok = True
+                for l in self.links:
+                    vals = nv.nvmlDeviceGetFieldValues(self.h, [(tx_id, l), (rx_id, l)])
+                    if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
+                        ok = False
+                        self.err = f"{name}: nvmlReturn {vals[0].nvmlReturn}/{vals[1].nvmlReturn}"
+                        break
+                    tx += vals[0].value.ullVal
+                    rx += vals[1].value.ullVal
+                if ok:
+                    self.field = name
+                    return scale * tx, scale * rx
+            except Exception as exc:
+                self.err = f"{name}: {exc}"
+        return None
 
 
 def cores():
@@ -620,9 +632,11 @@ def main():
         del A_host
 
     nvl = None
+    if nvlink is not None and "nvlink_tx" not in r:
+        nvl = {"unavailable": nvlink.err}
     if "nvlink_tx" in r:
         alg = fused_nvlink_bytes(cx, P) * args.steps
-        nvl = {"tx_bytes_all_ranks": r["nvlink_tx"], "rx_bytes_all_ranks": r["nvlink_rx"],
+        nvl = {"counter": nvlink.field, "tx_bytes_all_ranks": r["nvlink_tx"], "rx_bytes_all_ranks": r["nvlink_rx"],
                "algorithmic_bytes_all_ranks": alg,
                "tx_over_algorithmic": r["nvlink_tx"] / alg if alg else None,
                "note": "NVML NVLink data counters around the timed steps (filter + QR: the QR's Gram "

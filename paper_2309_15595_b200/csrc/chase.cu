@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -188,11 +189,20 @@ struct chase_handle_s {
   }
 };
 
+// NVTX range around a host scope (an API call or a phase); free when no tool is attached
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+static const char* const kCatName[CAT_N] = {"hemm_odd (A^H C -> B)", "hemm_even (A B -> C)", "allreduce",
+                                            "gram", "potrf", "trsm", "other", "hhqr"};
+
 struct ProfScope {
   chase_handle_s* h;
   int cat;
   cudaEvent_t a = nullptr;
-  ProfScope(chase_handle_s* h_, int c, int nlaunch) : h(h_), cat(c) {
+  Nvtx range;
+  ProfScope(chase_handle_s* h_, int c, int nlaunch) : h(h_), cat(c), range(kCatName[c]) {
     h->launches[c] += nlaunch;
     if (h->profiling) {
       a = h->ev_get();
@@ -302,8 +312,6 @@ static WsLayout ws_layout(const chase_handle_s* h) {
 
 
 // ==================================================================== GEMM launchers
-static bool g_fused_attr[2] = {false, false};
-static bool g_dfused_attr[2] = {false, false};
 static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B switch for tuning
 
 // (dynamic shared memory sizes of every variant are set once by preload_kernels)
@@ -333,7 +341,7 @@ static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorM
 
 static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                          const CUtensorMap& tX, const struct GemmReq& r,
-                                         const FusedArgs& f, int T);
+                                         const FusedArgs& f, int T, bool narrow);
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0,
@@ -432,7 +440,7 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
 
 static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                          const CUtensorMap& tX, const GemmReq& r,
-                                         const FusedArgs& f, int T) {
+                                         const FusedArgs& f, int T, bool narrow) {
   DGemmArgs a{};
   a.M = r.M; a.N = r.N; a.K = r.K;
   a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
@@ -443,18 +451,13 @@ static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CU
   a.band_map = r.band_map;
   a.a3d = r.a3d;
   const int grid = std::min(T, h->sm_budget > 0 ? std::min(h->sm_budget, h->num_sms) : h->num_sms);
-  if (trans) {
-    if (!g_dfused_attr[1]) {
-      CUDA_TRY(cudaFuncSetAttribute(dgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
-      g_dfused_attr[1] = true;
-    }
-    dgemm_fused_kernel<true><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  constexpr int S = dg_smem_bytes(DG_BN), SN = dg_smem_bytes(DG_BN_NARROW);
+  if (narrow) {
+    if (trans) dgemm_fused_kernel<true, DG_BN_NARROW><<<grid, DG_THREADS, SN, h->stream>>>(tA, tX, a, f);
+    else dgemm_fused_kernel<false, DG_BN_NARROW><<<grid, DG_THREADS, SN, h->stream>>>(tA, tX, a, f);
   } else {
-    if (!g_dfused_attr[0]) {
-      CUDA_TRY(cudaFuncSetAttribute(dgemm_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DG_SMEM_BYTES));
-      g_dfused_attr[0] = true;
-    }
-    dgemm_fused_kernel<false><<<grid, DG_THREADS, DG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+    if (trans) dgemm_fused_kernel<true><<<grid, DG_THREADS, S, h->stream>>>(tA, tX, a, f);
+    else dgemm_fused_kernel<false><<<grid, DG_THREADS, S, h->stream>>>(tA, tX, a, f);
   }
   CUDA_TRY(cudaGetLastError());
   return CHASE_OK;
@@ -561,9 +564,9 @@ static chase_status_t run_gemm_tail(chase_handle_s* h, const GemmReq& g) {
 
 static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                          const CUtensorMap& tX, const GemmReq& r,
-                                         const FusedArgs& f, int T) {
+                                         const FusedArgs& f, int T, bool narrow) {
   if (r.M <= 0 || r.N <= 0) return CHASE_OK;
-  if (h->dt == CHASE_R64) return launch_dgemm_fused(h, conj, tA, tX, r, f, T);
+  if (h->dt == CHASE_R64) return launch_dgemm_fused(h, conj, tA, tX, r, f, T, narrow);
   ZGemmArgs a{};
   a.M = r.M; a.N = r.N; a.K = r.K;
   a.a_d0 = r.a_d0; a.a_d1 = r.a_d1; a.x_k0 = r.x_k0; a.x_n0 = r.x_n0;
@@ -574,18 +577,13 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
   a.band_map = r.band_map;
   a.a3d = r.a3d;
   const int grid = std::min(T, h->sm_budget > 0 ? std::min(h->sm_budget, h->num_sms) : h->num_sms);
-  if (conj) {
-    if (!g_fused_attr[1]) {
-      CUDA_TRY(cudaFuncSetAttribute(zgemm_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
-      g_fused_attr[1] = true;
-    }
-    zgemm_fused_kernel<true><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+  constexpr int S = ZG_SMEM_BYTES, SN = zg_smem_bytes(ZG_BN_NARROW);
+  if (narrow) {
+    if (conj) zgemm_fused_kernel<true, ZG_BN_NARROW><<<grid, ZG_THREADS, SN, h->stream>>>(tA, tX, a, f);
+    else zgemm_fused_kernel<false, ZG_BN_NARROW><<<grid, ZG_THREADS, SN, h->stream>>>(tA, tX, a, f);
   } else {
-    if (!g_fused_attr[0]) {
-      CUDA_TRY(cudaFuncSetAttribute(zgemm_fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ZG_SMEM_BYTES));
-      g_fused_attr[0] = true;
-    }
-    zgemm_fused_kernel<false><<<grid, ZG_THREADS, ZG_SMEM_BYTES, h->stream>>>(tA, tX, a, f);
+    if (conj) zgemm_fused_kernel<true><<<grid, ZG_THREADS, S, h->stream>>>(tA, tX, a, f);
+    else zgemm_fused_kernel<false><<<grid, ZG_THREADS, S, h->stream>>>(tA, tX, a, f);
   }
   CUDA_TRY(cudaGetLastError());
   return CHASE_OK;
@@ -692,7 +690,9 @@ static FusedLayout fused_layout(const chase_handle_s* h) {
   L.ldb = pad_ld(nc_max);
   L.ldpo = L.ldb;
   L.ldpe = L.ldc;
-  L.tiles_max = ((rows_max + ZG_BM - 1) / ZG_BM) * ((h->n_max + ZG_BN - 1) / ZG_BN);
+  // tiles of the largest step (complex 128 x 64 tiles; real ones are no smaller) plus the narrow
+  // remainder tiles of a split step (at most 4 per m-tile)
+  L.tiles_max = ((rows_max + ZG_BM - 1) / ZG_BM) * ((h->n_max + ZG_BN - 1) / ZG_BN + 4);
   size_t off = 0;
   L.cw = off;
   off += align256((size_t)L.ldc * h->n_max * 16);
@@ -741,8 +741,12 @@ static chase_status_t preload_kernels() {
     ok &= smem((const void*)dgemm_kernel<false, true>, dg_smem_bytes(DG_BN));
     ok &= smem((const void*)zgemm_fused_kernel<true>, ZG_SMEM_BYTES);
     ok &= smem((const void*)zgemm_fused_kernel<false>, ZG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_fused_kernel<true>, DG_SMEM_BYTES);
-    ok &= smem((const void*)dgemm_fused_kernel<false>, DG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_fused_kernel<true>, dg_smem_bytes(DG_BN));
+    ok &= smem((const void*)dgemm_fused_kernel<false>, dg_smem_bytes(DG_BN));
+    ok &= smem((const void*)dgemm_fused_kernel<true, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)dgemm_fused_kernel<false, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)zgemm_fused_kernel<true, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
+    ok &= smem((const void*)zgemm_fused_kernel<false, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
     ok &= smem((const void*)fused_wait_kernel, 0);
     ok &= smem((const void*)zgemm_kernel<true, false, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
     ok &= smem((const void*)zgemm_kernel<false, false, ZG_BN_NARROW>, zg_smem_bytes(ZG_BN_NARROW));
@@ -1121,6 +1125,7 @@ chase_status_t chase_filter_record(chase_handle_t h, int32_t max_steps, chase_st
 chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, void* V,
                             int64_t ldv, int64_t ncols, const int32_t* degrees, double c,
                             double e, const chase_bounds_t* bounds, chase_stats_t* stats) {
+  Nvtx nv_("chase_filter");
   if (!h || !A_local || !V || !bounds) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max) return CHASE_EINVAL;
   if (lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
@@ -1258,22 +1263,51 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       }
       f.ldP = odd ? FL.ldpo : FL.ldpe;
       f.slot = (long long)f.ldP * h->n_max;
-      f.ep = ++h->fused_ep;
       f.done_target = h->fused_delivered;
       f.owner_beta = s > 1 ? 1 : 0;
       f.err = h->d_err;
       static const bool plain = getenv("CHASE_FUSED_PLAIN") != nullptr;
       f.plain = (m == 1 && plain) ? 1 : 0;
       f.tile_ctr = reinterpret_cast<unsigned long long*>(h->fz_base[me_world] + FL.ctr);
-      f.ctr_base = 0;                        // local counter, reset per launch (stream-ordered):
-      CUDA_TRY(cudaMemsetAsync(f.tile_ctr, 0, sizeof(unsigned long long), h->stream));   // CTAs
-      //   grab ahead, so the number of grabs per launch is not fixed
+      f.ctr_base = 0;                        // local counter, reset per launch (stream-ordered;
+      //                                        CTAs grab ahead, so grabs per launch vary)
       g.use_beta = 0;                        // the tile owner adds beta * old after the sum
-      const int BMf = h->dt == CHASE_C128 ? ZG_BM : DG_BM, BNf = h->dt == CHASE_C128 ? ZG_BN : DG_BN;
-      const int T = ((g.M + BMf - 1) / BMf) * ((g.N + BNf - 1) / BNf);
-      ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, 1);
-      STATUS_TRY(launch_zgemm_fused(h, g.conj, *g.tA, *g.tX, g, f, T));
-      h->fused_delivered += (unsigned long long)T;
+      const bool cplx = h->dt == CHASE_C128;
+      const int BMf = cplx ? ZG_BM : DG_BM, BNf = cplx ? ZG_BN : DG_BN;
+      const int BNn = cplx ? ZG_BN_NARROW : DG_BN_NARROW;
+      // ragged width: the N mod BN remainder columns as a second, narrow-tile fused launch when
+      // that pads less (own tile-index and staging-column ranges, so the two launches of the step
+      // never share a flag or a slot)
+      static const bool no_narrow = getenv("CHASE_NO_NARROW") != nullptr;
+      const int rem = g.N % BNf;
+      const bool split_w = !no_narrow && rem != 0 && (rem + BNn - 1) / BNn * BNn < BNf;
+      const int Nmain = split_w ? g.N - rem : g.N;
+      ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, split_w && Nmain > 0 ? 2 : 1);
+      int tile_base = 0;
+      for (int part = 0; part < (split_w ? 2 : 1); ++part) {
+        GemmReq gp = g;
+        const bool nar = part == 1;
+        FusedArgs fp = f;
+        if (nar) {
+          gp.N = rem;
+          gp.tX = g.tX_narrow;
+          gp.x_n0 = g.x_n0 + Nmain;
+          gp.xin = static_cast<const char*>(g.xin) + (size_t)Nmain * g.ldx * es;
+          for (int i = 0; i < m; ++i) fp.out[i] = reinterpret_cast<double2*>(
+              reinterpret_cast<char*>(f.out[i]) + (size_t)Nmain * g.ldo * es);
+          fp.col_base = Nmain;
+        } else {
+          gp.N = Nmain;
+        }
+        if (gp.N <= 0) continue;
+        const int T = ((gp.M + BMf - 1) / BMf) * ((gp.N + (nar ? BNn : BNf) - 1) / (nar ? BNn : BNf));
+        fp.tile_base = tile_base;
+        fp.ep = ++h->fused_ep;
+        CUDA_TRY(cudaMemsetAsync(f.tile_ctr, 0, sizeof(unsigned long long), h->stream));
+        STATUS_TRY(launch_zgemm_fused(h, gp.conj, *gp.tA, *gp.tX, gp, fp, T, nar));
+        tile_base += T;
+        h->fused_delivered += (unsigned long long)T;
+      }
       continue;
     }
     if (fused) {
@@ -1627,6 +1661,7 @@ extern "C" {
 
 chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols,
                             double cond_est, chase_stats_t* stats, int32_t* info_out) {
+  Nvtx nv_("chase_cholqr");
   if (!h || !V) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
   if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;   // TMA pitch
@@ -1707,6 +1742,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
 }
 
 chase_status_t chase_hhqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncols) {
+  Nvtx nv_("chase_hhqr");
   if (!h || !V) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max || ldv < h->n_r) return CHASE_EINVAL;
   if (((size_t)ldv * esize_of(h->dt)) % 16) return CHASE_EINVAL;
@@ -1794,6 +1830,7 @@ static chase_status_t redistribute_b2(chase_handle_s* h, const void* V, int64_t 
 // Alg.2 l.23-28: residual norms ||H v_j - lambda_j v_j|| of Ritz pairs.
 chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t lda, const void* V,
                                int64_t ldv, int64_t ncols, const double* ritz, double* resid) {
+  Nvtx nv_("chase_residuals");
   if (!h || !A_local || !V || !ritz || !resid) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
   for (int64_t j = 0; j < ncols; ++j)
@@ -1853,6 +1890,7 @@ chase_status_t chase_residuals(chase_handle_t h, const void* A_local, int64_t ld
 // Alg.2 l.16-22: Rayleigh-Ritz on the orthonormal C-layout block V.
 chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_t lda, void* V,
                                    int64_t ldv, int64_t ncols, double* ritz, int32_t* sweeps_out) {
+  Nvtx nv_("chase_rayleigh_ritz");
   if (!h || !A_local || !V || !ritz) return CHASE_EINVAL;
   if (ncols < 1 || ncols > h->n_max || lda < h->n_r || ldv < h->n_r) return CHASE_EINVAL;
   if (!h->ws || (h->virt && h->p * h->q > 1)) return CHASE_ESTATE;

@@ -1,6 +1,6 @@
 // dgemm_fused.cuh -- the real-symmetric filter step as ONE kernel (BASELINE C5 is real, P:76
-// "templated for complex/real type"): the dgemm mainloop (dgemm.cuh: 128 x 128 tiles, 16 k per
-// stage, XOR-linear k permutation) inside the persistent push/owner/broadcast protocol of
+// "templated for complex/real type"): the dgemm mainloop (dgemm.cuh: 128 x BN tiles, DG_KS
+// 16-k slabs per stage, XOR-linear k permutation) inside the persistent push/owner/broadcast protocol of
 // zgemm_fused.cuh (dynamic tile scheduler, partial tiles pushed into the owner's staging slots
 // over NVLink, fixed-order owner sum + beta term, broadcast, delivery counters, bounded spins).
 // See zgemm_fused.cuh for the protocol and its deadlock-freedom argument; only the element type
@@ -11,23 +11,26 @@
 
 namespace chase {
 
-template <bool TRANS>
+template <bool TRANS, int BN_ = DG_BN>
 __global__ void __launch_bounds__(DG_THREADS, 1)
     dgemm_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                        const DGemmArgs g, const FusedArgs f) {
+  constexpr int WN_ = BN_ / 2, NT_ = WN_ / 8;                     // warp tile columns, n8 tiles
+  constexpr int SLA = DG_BM * DG_BK * 8, SLX = BN_ * DG_BK * 8;   // one k-slab of A / X
+  constexpr int AB_ = DG_KS * SLA, SB_ = DG_KS * (SLA + SLX), ST_ = dg_stages(BN_);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + DG_STAGES * DG_STAGE_BYTES);
-  uint64_t* empty = full + DG_STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST_ * SB_);
+  uint64_t* empty = full + ST_;
   __shared__ int s_abort;
   __shared__ int s_q[FUSED_QCAP];
   __shared__ int s_qh, s_qt, s_cmd;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = (g.N + DG_BN - 1) / DG_BN, m_tiles = (g.M + DG_BM - 1) / DG_BM;
+  const int n_tiles = (g.N + BN_ - 1) / BN_, m_tiles = (g.M + DG_BM - 1) / DG_BM;
   const int T = n_tiles * m_tiles;
-  const int KT = (g.K + DG_BK - 1) / DG_BK;
-  constexpr int RING = DG_STAGES + 4;                  // see zgemm_fused.cuh (grab 2 ahead)
+  const int KT = (g.K + DG_BKT - 1) / DG_BKT;
+  constexpr int RING = ST_ + 4;                  // see zgemm_fused.cuh (grab 2 ahead)
   __shared__ int s_tile[RING];
   auto grab = [&]() -> int {
     const unsigned long long v = atomicAdd(f.tile_ctr, 1ull) - f.ctr_base;
@@ -39,7 +42,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     const int gm = min(DG_GROUP_M, m_tiles - first_m);
     const int within = t - group * DG_GROUP_M * n_tiles;
     m0 = (first_m + within % gm) * DG_BM;
-    n0 = (within / gm) * DG_BN;
+    n0 = (within / gm) * BN_;
   };
 
   if (threadIdx.x == 0) {
@@ -57,7 +60,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       }
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int s = 0; s < DG_STAGES; ++s) {
+    for (int s = 0; s < ST_; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], DG_CONSUMERS);
     }
@@ -78,49 +81,53 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     }
     int m0, n0;
     tile_origin(t, m0, n0);
-    const int k0 = (q % KT) * DG_BK;
-    mbar_arrive_expect_tx(&full[s], DG_STAGE_BYTES);
-    uint8_t* sa = smem + s * DG_STAGE_BYTES;
-    uint8_t* sx = sa + DG_A_BYTES;
-    if (TRANS) {
-      tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);
-    } else if (g.a3d) {
-      tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 16, &full[s]);
-    } else {
+    mbar_arrive_expect_tx(&full[s], SB_);
 #pragma unroll
-      for (int b = 0; b < DG_BM / 16; ++b)
-        tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+    for (int u = 0; u < DG_KS; ++u) {
+      const int k0 = (q % KT) * DG_BKT + u * DG_BK;
+      uint8_t* sa = smem + s * SB_ + u * SLA;
+      uint8_t* sx = smem + s * SB_ + AB_ + u * SLX;
+      if (TRANS) {
+        tma_load_2d(sa, &tmA, g.a_d0 + k0, g.a_d1 + m0, &full[s]);
+      } else if (g.a3d) {
+        tma_load_3d(sa, &tmA, 0, g.a_d1 + k0, (g.a_d0 + m0) / 16, &full[s]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < DG_BM / 16; ++b)
+          tma_load_2d(sa + b * 2048, &tmA, g.a_d0 + m0 + 16 * b, g.a_d1 + k0, &full[s]);
+      }
+      tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);
     }
-    tma_load_2d(sx, &tmX, g.x_k0 + k0, g.x_n0 + n0, &full[s]);
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmX);
     for (int sq = 0; sq * KT < 2; ++sq) s_tile[sq % RING] = grab();
-    for (int gs = 0; gs < DG_STAGES; ++gs) issue(gs, gs);
+    for (int gs = 0; gs < ST_; ++gs) issue(gs, gs);
   }
 
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  double acc[DG_MT][DG_NT][4];
+  double acc[DG_MT][NT_][4];
   auto zero_acc = [&]() {
 #pragma unroll
     for (int i = 0; i < DG_MT; ++i)
 #pragma unroll
-      for (int j = 0; j < DG_NT; ++j)
+      for (int j = 0; j < NT_; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
   };
   zero_acc();
 
-  constexpr int SUBS = DG_BK / 4;
+  constexpr int SUBS = DG_BKT / 4;
   struct Frag {
-    double a[DG_MT][2], b[DG_NT];
+    double a[DG_MT][2], b[NT_];
   };
-  auto load = [&](Frag& fr, int gs, int kt, int hsub) {
+  auto load = [&](Frag& fr, int gs, int kt, int sub) {
+    const int u = sub >> 2, hsub = sub & 3;
     const int k = dg_kperm(tq, hsub);
-    const uint8_t* sa = smem + (gs % DG_STAGES) * DG_STAGE_BYTES;
-    const uint8_t* sx = sa + DG_A_BYTES;
+    const uint8_t* sa = smem + (gs % ST_) * SB_ + u * SLA;
+    const uint8_t* sx = smem + (gs % ST_) * SB_ + AB_ + u * SLX;
 #pragma unroll
     for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
@@ -132,15 +139,15 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         fr.a[mt][r] = *reinterpret_cast<const double*>(sa + off);
       }
 #pragma unroll
-    for (int nt = 0; nt < DG_NT; ++nt) {
-      const int n = wn * DG_WN + nt * 8 + gq;
+    for (int nt = 0; nt < NT_; ++nt) {
+      const int n = wn * WN_ + nt * 8 + gq;
       fr.b[nt] = *reinterpret_cast<const double*>(sx + n * 128 + ((((k >> 1) ^ gq) << 4) | ((k & 1) << 3)));
     }
-    if (kt * DG_BK + k >= g.K) {
+    if (kt * DG_BKT + u * DG_BK + k >= g.K) {
 #pragma unroll
       for (int mt = 0; mt < DG_MT; ++mt) fr.a[mt][0] = fr.a[mt][1] = 0.0;
 #pragma unroll
-      for (int nt = 0; nt < DG_NT; ++nt) fr.b[nt] = 0.0;
+      for (int nt = 0; nt < NT_; ++nt) fr.b[nt] = 0.0;
     }
   };
 
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     tile_origin(t, m0, n0);
     double* const* outs = reinterpret_cast<double* const*>(f.out);
     const double* __restrict__ mine = reinterpret_cast<const double*>(f.P[f.me]);
-    constexpr int PER = DG_BM * DG_BN / DG_THREADS;     // 64 elements per thread
+    constexpr int PER = DG_BM * BN_ / DG_THREADS;     // 64 elements per thread
     constexpr int BATCH = 8;
 #pragma unroll 1
     for (int b0 = 0; b0 < PER; b0 += BATCH) {
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         const int e = threadIdx.x + (b0 + i) * DG_THREADS;
         const int row = m0 + (e % DG_BM), col = n0 + (e / DG_BM);
         ok[i] = row < g.M && col < g.N;
-        const long long ip = (long long)row + (long long)col * f.ldP;
+        const long long ip = (long long)row + (long long)(f.col_base + col) * f.ldP;
         io[i] = (long long)row + (long long)col * g.ldo;
         sum[i] = ok[i] ? mine[ip] : 0.0;
         for (int src = 1; src < f.m; ++src) sum[i] += ok[i] ? mine[(long long)src * f.slot + ip] : 0.0;
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   // an owner that still has tiles to compute.
   auto flags_ready = [&](int t) -> bool {      // thread 0
     for (int src = 0; src < f.m; ++src)
-      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) return false;
+      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)(f.tile_base + t) * f.m + src) != f.ep) return false;
     return true;
   };
   auto drain = [&](bool final_) {
@@ -202,8 +209,8 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
               __nanosleep(64);
               if (clock64() - t0 > FUSED_SPIN_CYCLES) {
                 printf("[chase fused] member %d CTA %d: tile %d partials missing (m %d, ep %u, flags %u %u, final %d, q %d..%d)\n",
-                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)t * f.m],
-                       f.flags[f.me][(long long)t * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
+                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)(f.tile_base + t) * f.m],
+                       f.flags[f.me][(long long)(f.tile_base + t) * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
                 atomicExch(f.err, 1);
                 s_abort = 1;
                 break;
@@ -233,11 +240,11 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
 #pragma unroll
       for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < DG_NT; ++nt)
+        for (int nt = 0; nt < NT_; ++nt)
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int row = m0 + wm * DG_WM + mt * 16 + gq + ((r & 2) ? 8 : 0);
-            const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
+            const int col = n0 + wn * WN_ + nt * 8 + 2 * tq + (r & 1);
             if (row < g.M && col < g.N) {
               double v = acc[mt][nt][r];
               if (row >= g.band_lo && row < g.band_hi)
@@ -251,27 +258,27 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       if (threadIdx.x == 0) atomicAdd(f.done[f.me], 1ull);
       return;
     }
-    const int owner = t % f.m;
+    const int owner = (f.tile_base + t) % f.m;
     double* slot = reinterpret_cast<double*>(f.P[owner]) + (long long)f.me * f.slot;
 #pragma unroll
     for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < DG_NT; ++nt)
+      for (int nt = 0; nt < NT_; ++nt)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int row = m0 + wm * DG_WM + mt * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = n0 + wn * DG_WN + nt * 8 + 2 * tq + (r & 1);
+          const int col = n0 + wn * WN_ + nt * 8 + 2 * tq + (r & 1);
           if (row < g.M && col < g.N) {
             double v = acc[mt][nt][r];
             const int bsrc = g.band_map != nullptr ? g.band_map[row]
                              : (row >= g.band_lo && row < g.band_hi ? row + g.band_shift : -1);
             if (bsrc >= 0) v -= g.c * g.xin[(long long)bsrc + (long long)col * g.ldx];
-            slot[(long long)row + (long long)col * f.ldP] = v * g.alpha;
+            slot[(long long)row + (long long)(f.col_base + col) * f.ldP] = v * g.alpha;
           }
         }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
+    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)(f.tile_base + t) * f.m + f.me, f.ep);
     if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
       s_q[s_qt % FUSED_QCAP] = t;
       ++s_qt;
@@ -286,7 +293,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   load(cur, 0, 0, 0);
   int seq = 0, kt = 0, gs = 0;
   for (;;) {
-    const int s = gs % DG_STAGES;
+    const int s = gs % ST_;
     int next_tile = tile;
 #pragma unroll
     for (int sub = 0; sub < SUBS; ++sub) {
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        mbar_wait_dbg(&full[(gs + 1) % DG_STAGES], ((gs + 1) / DG_STAGES) & 1, 2, gs);
+        mbar_wait_dbg(&full[(gs + 1) % ST_], ((gs + 1) / ST_) & 1, 2, gs);
         if (kt + 1 < KT) {
           load(nxt, gs + 1, kt + 1, 0);
         } else {
@@ -306,13 +313,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
 #pragma unroll
       for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < DG_NT; ++nt) dmma_16x8x4(acc[mt][nt], cur.a[mt][0], cur.a[mt][1], cur.b[nt]);
+        for (int nt = 0; nt < NT_; ++nt) dmma_16x8x4(acc[mt][nt], cur.a[mt][0], cur.a[mt][1], cur.b[nt]);
       cur = nxt;
     }
     if (lane == 0 && warp == (gs & (DG_CONSUMERS - 1)) && gs >= 1) {
-      const int sp = (gs - 1) % DG_STAGES;
-      mbar_wait_dbg(&empty[sp], ((gs - 1) / DG_STAGES) & 1, 3, gs);
-      issue(gs - 1 + DG_STAGES, sp);
+      const int sp = (gs - 1) % ST_;
+      mbar_wait_dbg(&empty[sp], ((gs - 1) / ST_) & 1, 3, gs);
+      issue(gs - 1 + ST_, sp);
     }
     ++gs;
     if (++kt == KT) {
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       zero_acc();
       if (s_abort) {
         if (threadIdx.x == 0)
-          for (int r = gs; r < gs + DG_STAGES - 1; ++r) mbar_wait(&full[r % DG_STAGES], (r / DG_STAGES) & 1);
+          for (int r = gs; r < gs + ST_ - 1; ++r) mbar_wait(&full[r % ST_], (r / ST_) & 1);
         return;
       }
       kt = 0;

@@ -52,6 +52,10 @@ struct FusedArgs {
   int plain;                                 // diagnostics: local epilogue, no protocol (m == 1)
   unsigned long long* tile_ctr;              // dynamic tile scheduler (monotonic, local)
   unsigned long long ctr_base;               // value of *tile_ctr at launch start (0: reset per launch)
+  int tile_base;                             // flag index / owner offset of this launch's tiles
+  int col_base;                              // staging-slot column offset of this launch's tiles
+                                             //   (a step split into a wide-tile launch and a
+                                             //   narrow-tile remainder launch keeps the two apart)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
@@ -69,20 +73,22 @@ __device__ __forceinline__ void st_release_sys_u32(unsigned* p, unsigned v) {
 }
 constexpr long long FUSED_SPIN_CYCLES = 20000000000LL;   // ~10 s at 2 GHz
 
-template <bool CONJ>
+template <bool CONJ, int BN_ = ZG_BN>
 __global__ void __launch_bounds__(ZG_THREADS, 1)
     zgemm_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                        const ZGemmArgs g, const FusedArgs f) {
+  constexpr int WN_ = BN_ / ZG_WNW, NT_ = WN_ / 8;
+  constexpr int XS_ = BN_ * 8 * 16, XB_ = XS_ * ZG_KS, SB_ = ZG_A_BYTES + XB_;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * ZG_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ZG_STAGES * SB_);
   uint64_t* empty = full + ZG_STAGES;
   __shared__ int s_abort;
   __shared__ int s_q[FUSED_QCAP];
   __shared__ int s_qh, s_qt, s_cmd;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = (g.N + ZG_BN - 1) / ZG_BN, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
+  const int n_tiles = (g.N + BN_ - 1) / BN_, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
   const int T = n_tiles * m_tiles;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
   // dynamic tile scheduler: tiles come from a global counter into a small smem ring (tile -1 =
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     const int gm = min(ZG_GROUP_M, m_tiles - first_m);
     const int within = t - group * ZG_GROUP_M * n_tiles;
     m0 = (first_m + within % gm) * ZG_BM;
-    n0 = (within / gm) * ZG_BN;
+    n0 = (within / gm) * BN_;
   };
 
   if (threadIdx.x == 0) {
@@ -144,8 +150,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     int m0, n0;
     tile_origin(t, m0, n0);
     const int kt = q % KT;
-    mbar_arrive_expect_tx(&full[s], ZG_STAGE_BYTES);
-    uint8_t* sa = smem + s * ZG_STAGE_BYTES;
+    mbar_arrive_expect_tx(&full[s], SB_);
+    uint8_t* sa = smem + s * SB_;
     uint8_t* sx = sa + ZG_A_BYTES;
 #pragma unroll
     for (int u = 0; u < ZG_KS; ++u) {
@@ -160,7 +166,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         for (int b = 0; b < ZG_BM / 8; ++b)
           tma_load_2d(sau + b * 1024, &tmA, 2 * (g.a_d0 + m0 + 8 * b), g.a_d1 + k0, &full[s]);
       }
-      tma_load_2d(sx + u * ZG_X_SLAB, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
+      tma_load_2d(sx + u * XS_, &tmX, 2 * (g.x_k0 + k0), g.x_n0 + n0, &full[s]);
     }
   };
   if (threadIdx.x == 0) {
@@ -172,12 +178,12 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   const int wm = warp & 3, wn = warp >> 2;
   const int gq = lane >> 2, tq = lane & 3;
-  double acc_re[2][ZG_NT][4], acc_im[2][ZG_NT][4];
+  double acc_re[2][NT_][4], acc_im[2][NT_][4];
   auto zero_acc = [&]() {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < ZG_NT; ++j)
+      for (int j = 0; j < NT_; ++j)
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc_re[i][j][r] = acc_im[i][j][r] = 0.0;
   };
@@ -185,13 +191,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   constexpr int SUBS = 2 * ZG_KS;
   struct Frag {
-    double2 a[2][2], b[ZG_NT];
+    double2 a[2][2], b[NT_];
   };
   auto load = [&](Frag& fr, int gs, int kt, int sub) {
     const int u = sub >> 1, h = sub & 1;
     const int k = 2 * tq + h;
-    const uint8_t* sa = smem + (gs % ZG_STAGES) * ZG_STAGE_BYTES + u * ZG_A_SLAB;
-    const uint8_t* sx = smem + (gs % ZG_STAGES) * ZG_STAGE_BYTES + ZG_A_BYTES + u * ZG_X_SLAB;
+    const uint8_t* sa = smem + (gs % ZG_STAGES) * SB_ + u * ZG_A_SLAB;
+    const uint8_t* sx = smem + (gs % ZG_STAGES) * SB_ + ZG_A_BYTES + u * XS_;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -201,29 +207,29 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         fr.a[mt][r] = *reinterpret_cast<const double2*>(sa + off);
       }
 #pragma unroll
-    for (int nt = 0; nt < ZG_NT; ++nt) {
-      const int n = wn * ZG_WN + nt * 8 + gq;
+    for (int nt = 0; nt < NT_; ++nt) {
+      const int n = wn * WN_ + nt * 8 + gq;
       fr.b[nt] = *reinterpret_cast<const double2*>(sx + n * 128 + ((k ^ gq) << 4));
     }
     if (kt * ZG_BK + 8 * u + k >= g.K) {
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) fr.a[mt][0] = fr.a[mt][1] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) fr.b[nt] = make_double2(0.0, 0.0);
+      for (int nt = 0; nt < NT_; ++nt) fr.b[nt] = make_double2(0.0, 0.0);
     }
   };
   auto mma = [&](const Frag& fr) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) {
+      for (int nt = 0; nt < NT_; ++nt) {
         dmma_16x8x4(acc_re[mt][nt], fr.a[mt][0].x, fr.a[mt][1].x, fr.b[nt].x);
         dmma_16x8x4(acc_im[mt][nt], fr.a[mt][0].x, fr.a[mt][1].x, fr.b[nt].y);
       }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt) {
+      for (int nt = 0; nt < NT_; ++nt) {
         const double bre = CONJ ? fr.b[nt].y : -fr.b[nt].y;
         const double bim = CONJ ? -fr.b[nt].x : fr.b[nt].x;
         dmma_16x8x4(acc_re[mt][nt], fr.a[mt][0].y, fr.a[mt][1].y, bre);
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
     // coalesced pass over the tile (column-major 128 x 64), partials read from local slots;
     // 8 elements per thread per batch so the loads of a batch are all in flight together
     const double2* __restrict__ mine = f.P[f.me];
-    constexpr int PER = ZG_BM * ZG_BN / ZG_THREADS;     // 32 elements per thread
+    constexpr int PER = ZG_BM * BN_ / ZG_THREADS;     // 32 elements per thread
     constexpr int BATCH = 8;
 #pragma unroll 1
     for (int b0 = 0; b0 < PER; b0 += BATCH) {
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         const int e = threadIdx.x + (b0 + i) * ZG_THREADS;
         const int row = m0 + (e % ZG_BM), col = n0 + (e / ZG_BM);
         ok[i] = row < g.M && col < g.N;
-        const long long ip = (long long)row + (long long)col * f.ldP;
+        const long long ip = (long long)row + (long long)(f.col_base + col) * f.ldP;
         io[i] = (long long)row + (long long)col * g.ldo;
         sum[i] = ok[i] ? mine[ip] : make_double2(0.0, 0.0);
         for (int src = 1; src < f.m; ++src) {
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   // an owner that still has tiles to compute.
   auto flags_ready = [&](int t) -> bool {      // thread 0
     for (int src = 0; src < f.m; ++src)
-      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)t * f.m + src) != f.ep) return false;
+      if (ld_acquire_sys_u32(f.flags[f.me] + (long long)(f.tile_base + t) * f.m + src) != f.ep) return false;
     return true;
   };
   auto drain = [&](bool final_) {
@@ -298,8 +304,8 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
               __nanosleep(64);
               if (clock64() - t0 > FUSED_SPIN_CYCLES) {
                 printf("[chase fused] member %d CTA %d: tile %d partials missing (m %d, ep %u, flags %u %u, final %d, q %d..%d)\n",
-                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)t * f.m],
-                       f.flags[f.me][(long long)t * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
+                       f.me, (int)blockIdx.x, t, f.m, f.ep, f.flags[f.me][(long long)(f.tile_base + t) * f.m],
+                       f.flags[f.me][(long long)(f.tile_base + t) * f.m + (f.m > 1 ? 1 : 0)], (int)final_, s_qh, s_qt);
                 atomicExch(f.err, 1);
                 s_abort = 1;
                 break;
@@ -329,11 +335,11 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < ZG_NT; ++nt)
+        for (int nt = 0; nt < NT_; ++nt)
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
-            const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
+            const int col = n0 + wn * WN_ + nt * 8 + 2 * tq + (r & 1);
             if (row < g.M && col < g.N) {
               double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
               if (row >= g.band_lo && row < g.band_hi) {
@@ -356,16 +362,16 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
       return;
     }
     // owner = t mod m: consecutive tiles (those in flight together) go to different members
-    const int owner = t % f.m;
+    const int owner = (f.tile_base + t) % f.m;
     double2* slot = f.P[owner] + (long long)f.me * f.slot;        // my slot at the owner
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < ZG_NT; ++nt)
+      for (int nt = 0; nt < NT_; ++nt)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int row = m0 + wm * 32 + mt * 16 + gq + ((r & 2) ? 8 : 0);
-          const int col = n0 + wn * ZG_WN + nt * 8 + 2 * tq + (r & 1);
+          const int col = n0 + wn * WN_ + nt * 8 + 2 * tq + (r & 1);
           if (row < g.M && col < g.N) {
             double vr = acc_re[mt][nt][r], vi = acc_im[mt][nt][r];
             const int bsrc = g.band_map != nullptr ? g.band_map[row]
@@ -375,12 +381,12 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
               vr -= g.c * x.x;
               vi -= g.c * x.y;
             }
-            slot[(long long)row + (long long)col * f.ldP] = make_double2(vr * g.alpha, vi * g.alpha);
+            slot[(long long)row + (long long)(f.col_base + col) * f.ldP] = make_double2(vr * g.alpha, vi * g.alpha);
           }
         }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)t * f.m + f.me, f.ep);
+    if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)(f.tile_base + t) * f.m + f.me, f.ep);
     if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
       s_q[s_qt % FUSED_QCAP] = t;
       ++s_qt;

@@ -10,7 +10,7 @@ torchrun).  Checks, on the same seeded inputs the bench uses:
   the column communicator) and the executed Alg.4 variant equal to the oracle's selection;
 * bookkeeping: the per-rank record equals the oracle's record.
 
-Usage (torchrun): python tests/full_worker.py CONFIG p q OUT.json
+Usage (torchrun): python tests/full_worker.py CONFIG p q OUT.json [fused|nccl]
 """
 import json
 import os
@@ -28,7 +28,7 @@ import paper_2309_15595_b200 as cb
 from cheb_closed_form import dft_phase_closed_form, hartley_closed_form
 
 
-def run_full(name, p, q, rank=0, local=0, dist=None, oracle_cols=True):
+def run_full(name, p, q, rank=0, local=0, dist=None, oracle_cols=True, mode="nccl"):
     cfg = ci.CONFIGS[name]
     N, n = cfg.N, cfg.n
     lam = cfg.spectrum_values()
@@ -42,6 +42,9 @@ def run_full(name, p, q, rank=0, local=0, dist=None, oracle_cols=True):
     dev = torch.device("cuda", local)
     h = cb.Chase(cb.CHASE_C128 if cfg.complex_ else cb.CHASE_R64, N, n, p, q, myrow, mycol, uid, local)
     n_r, n_c, r0, c0 = h.n_r, h.n_c, h.r0, h.c0
+    if mode == "fused" and dist is not None:
+        from paper_2309_15595_b200 import dist as cdist
+        cdist.enable_fused_comm(h)            # filter steps as fused HEMM + NVLink reduction
     gen = ci.dft_phase(lam, cfg.seed) if cfg.complex_ else ci.hartley_sign(lam, cfg.seed)
     A_t = gen.block(r0, n_r, c0, n_c, device=dev)
     V0 = ci.gaussian_block(N, n, cfg.seed + 1000, cfg.complex_)
@@ -50,7 +53,7 @@ def run_full(name, p, q, rank=0, local=0, dist=None, oracle_cols=True):
     rec, mv = h.record()
     torch.cuda.synchronize()
     Vf = V_t.cpu().numpy().T                                   # (n_r, n) of this rank
-    res = {"config": name, "grid": f"{p}x{q}", "rank": rank}
+    res = {"config": name, "grid": f"{p}x{q}", "rank": rank, "mode": mode}
 
     # FFT closed form on a spread of columns
     cols = np.unique(np.linspace(0, n - 1, 48).astype(int))
@@ -90,11 +93,12 @@ def run_full(name, p, q, rank=0, local=0, dist=None, oracle_cols=True):
 
 def main():
     name, p, q, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    mode = sys.argv[5] if len(sys.argv) > 5 else "nccl"
     import torch.distributed as dist
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    res = run_full(name, p, q, rank, local, dist)
+    res = run_full(name, p, q, rank, local, dist, mode=mode)
     g = [None] * dist.get_world_size()
     dist.all_gather_object(g, res)
     if rank == 0:

@@ -110,21 +110,25 @@ def test_grid_matches_oracle(tmp_path, grid, complex_, pad, mode, nb):
     assert np.linalg.norm(X.conj().T @ X - np.eye(n)) <= 1e-11
 
 
-FULL = [("C3", (2, 1)), ("C3", (2, 2)), ("C3", (2, 4)), ("C4", (2, 2)), ("C4", (2, 4)),
-        ("C5", (2, 2)), ("C5", (2, 4))]
+FULL = [(c, g, m) for c, g in [("C3", (2, 1)), ("C3", (2, 2)), ("C3", (2, 4)), ("C4", (2, 2)),
+                                ("C4", (2, 4)), ("C5", (2, 2)), ("C5", (1, 4)), ("C5", (4, 1)),
+                                ("C5", (2, 4))]
+        for m in ("fused", "nccl")]
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,grid", FULL)
-def test_full_size_grid(tmp_path, name, grid):
+@pytest.mark.parametrize("name,grid,mode", FULL)
+def test_full_size_grid(tmp_path, name, grid, mode):
     """BASELINE configurations on the 2D grid: closed-form filter check of sampled columns on every
-    rank, per-rank bookkeeping, Alg.4 variant and distributed orthogonality (tests/full_worker.py)."""
+    rank, per-rank bookkeeping, Alg.4 variant and distributed orthogonality (tests/full_worker.py),
+    with the filter steps as fused HEMM + NVLink reduction kernels or HEMM + ncclAllReduce."""
     import json
     p, q = grid
     if ngpus() < p * q:
         pytest.skip(f"needs {p * q} GPUs")
     out = str(tmp_path / "full.json")
-    r = torchrun(p * q, [os.path.join(ROOT, "tests", "full_worker.py"), name, str(p), str(q), out], 1800)
+    r = torchrun(p * q, [os.path.join(ROOT, "tests", "full_worker.py"), name, str(p), str(q), out,
+                         mode], 1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for res in json.load(open(out)):
         print(res)
