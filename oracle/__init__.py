@@ -14,6 +14,11 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``): closed-form Chebyshev values (c
 brute-force eigendecomposition for N <= 64, the FFT closed form of the DFT-phase matrices,
 SPEC's hand-computed examples under tests/golden/, QR invariants and LAPACK Householder QR.
 Every function here is pinned; none is "parity unpinned".
+
+``oracle/cpp/chase_oracle.cpp`` (binding ``oracle.cpp_oracle``) is the same filter and CholeskyQR
+family as plain C++17 triple loops with OpenMP over output rows (the north star's "plain, slow
+CPU filter and CholeskyQR with triple loops"), pinned by tests/test_oracle_cpp.py with the same
+closed forms and golden cases; bench.py times it as ``cpu_baseline`` and the reference arm.
 """
 from .filter import chebyshev_scalars, chebyshev_filter, filter_schedule, filter_record  # noqa: F401
 from .qr import (gram, potrf_upper, trsm_right_upper, shift_value, cholesky_qr, caqr,  # noqa: F401
