@@ -170,6 +170,7 @@ class NvLink:
     the Blackwell counters), else THROUGHPUT_DATA_TX/RX (KiB)."""
 
     def __init__(self, index: int):
+        self.index = index
         self.h, self.err, self.links = None, None, []
         try:
             import pynvml
@@ -189,7 +190,7 @@ class NvLink:
 
     def read(self):
         if self.h is None or not self.links:
-            return None
+            return self._smi()
         nv = self.nv
         for tx_id, rx_id, scale, name in (
                 (getattr(nv, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", None),
@@ -214,6 +215,27 @@ class NvLink:
                     return scale * tx, scale * rx
             except Exception as exc:
                 self.err = f"{name}: {exc}"
+        return self._smi()
+
+    def _smi(self):
+        """Fallback: `nvidia-smi nvlink -gt d` (per-link data Tx/Rx KiB counters)."""
+        try:
+            out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(self.index)],
+                                 capture_output=True, text=True, timeout=20).stdout
+            tx = rx = 0
+            seen = False
+            for line in out.splitlines():
+                parts = line.replace(":", " ").split()
+                if "Tx" in parts and "KiB" in parts:
+                    tx += int(parts[parts.index("KiB") - 1]); seen = True
+                elif "Rx" in parts and "KiB" in parts:
+                    rx += int(parts[parts.index("KiB") - 1]); seen = True
+            if seen:
+                self.field = "nvidia-smi nvlink -gt d"
+                return 1024 * tx, 1024 * rx
+            self.err = (self.err or "") + f"; nvidia-smi nvlink -gt d: no counters ({out.strip()[:80]!r})"
+        except Exception as exc:
+            self.err = (self.err or "") + f"; nvidia-smi nvlink: {exc}"
         return None
 
 
