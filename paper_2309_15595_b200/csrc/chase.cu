@@ -1405,20 +1405,16 @@ chase_status_t chase_filter_step(chase_handle_t h, const void* A_local, int64_t 
 // ==================================================================== CholeskyQR (Alg.3/4)
 namespace {
 
+// diagonal block kb: R_kk and R_kk^{-1} (into Rinv[:, kb:kb+64], ld 64)
 template <typename T>
-void potrf_blocks(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb, int n, int rest) {
-  potrf_diag_kernel<T><<<1, 256, diag_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info);
+void potrf_diag(chase_handle_s* h, char* G, int64_t ldg, int kb, int nb) {
+  potrf_diag_kernel<T><<<1, POTRF_DIAG_THREADS, diag_smem<T>(), h->stream>>>(
+      reinterpret_cast<T*>(G), ldg, kb, nb, h->d_info, reinterpret_cast<T*>(h->Rinv) + (size_t)kb * QR_NB);
   h->launches[CAT_POTRF]++;
-  if (rest > 0) {
-    potrf_panel_kernel<T><<<(rest + PANEL_THREADS - 1) / PANEL_THREADS, PANEL_BLOCK,
-                            panel_smem<T>(), h->stream>>>(reinterpret_cast<T*>(G), ldg, kb, nb, n,
-                                                          h->d_info);
-    h->launches[CAT_POTRF]++;
-  }
 }
 
 struct QrMaps {
-  CUtensorMap vA_t, vA_nt, vX, gA_t, gX, wA_nt, rinvX;
+  CUtensorMap vA_t, vA_nt, vX, gA_t, gX, wA_nt, rinvX, rinvA_t;
   CUtensorMap gA_nt, rfA_nt, rfX, tmpX;      // TRSM through R^{-1} (recursive doubling)
   int v_a3d = 0, w_a3d = 0;
 };
@@ -1502,10 +1498,22 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
       const int nb = std::min(QR_NB, n - kb);
       const int rest = n - kb - nb;
       if (h->dt == CHASE_C128)
-        potrf_blocks<double2>(h, G, ldg, kb, nb, n, rest);
+        potrf_diag<double2>(h, G, ldg, kb, nb);
       else
-        potrf_blocks<double>(h, G, ldg, kb, nb, n, rest);
+        potrf_diag<double>(h, G, ldg, kb, nb);
       CUDA_TRY(cudaGetLastError());
+      if (rest > 0) {
+        // block row R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:] on the tensor cores, in place (one
+        // m-tile: every CTA reads only the columns it writes, all its k-tiles before its epilogue)
+        GemmReq g{};
+        g.conj = true; g.tA = &mp.rinvA_t; g.tX = &mp.gX;
+        g.M = nb; g.N = rest; g.K = nb;
+        g.a_d0 = 0; g.a_d1 = kb; g.x_k0 = kb; g.x_n0 = kb + nb;
+        g.out = G + ((size_t)kb + (size_t)(kb + nb) * ldg) * es; g.ldo = ldg;
+        g.alpha = 1.0; g.abort_flag = h->d_info;
+        STATUS_TRY(run_gemm(h, g));
+        h->launches[CAT_POTRF]++;
+      }
       if (rest > 0) {
         // trailing HERK: G[j, l] -= sum_a conj(R[a, j]) R[a, l], a in the panel, j <= l
         GemmReq g{};
@@ -1669,12 +1677,10 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   if (!h->ws || (h->virt && h->p > 1)) return CHASE_ESTATE;
   if (reinterpret_cast<uintptr_t>(V) & 15) return CHASE_EINVAL;
   if (!g_qr_attr_done) {
-    CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double2>()));
     CUDA_TRY(cudaFuncSetAttribute(trtri_diag_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, trtri_smem<double2>()));
     CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<double2>()));
     CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem<double>()));
     CUDA_TRY(cudaFuncSetAttribute(trtri_diag_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, trtri_smem<double>()));
-    CUDA_TRY(cudaFuncSetAttribute(potrf_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_smem<double>()));
     g_qr_attr_done = true;
   }
   const int n = (int)ncols;
@@ -1686,6 +1692,7 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
   STATUS_TRY(make_role_map(h, &mp.gX, h->Gws, n, n, pad_ld(n), ROLE_X));
   STATUS_TRY(make_role_map(h, &mp.wA_nt, h->Wws, h->n_r, n, pad_ld(h->n_r), ROLE_A_NOTRANS, &mp.w_a3d));
   STATUS_TRY(make_role_map(h, &mp.rinvX, h->Rinv, TRTRI_NB, n, TRTRI_NB, ROLE_X));
+  STATUS_TRY(make_role_map(h, &mp.rinvA_t, h->Rinv, TRTRI_NB, n, TRTRI_NB, ROLE_A_TRANS));
   {
     char* Rf = h->Rfws;
     char* Tmp = h->Rfws + align256((size_t)pad_ld(h->n_max) * h->n_max * esize_of(h->dt));

@@ -3,8 +3,8 @@
 // flop-heavy pieces (Gram X^H X, the trailing HERK update of the blocked POTRF, the TRSM
 // diagonal-block products and right-looking updates) run on the tensor-core GEMMs.
 //
-//   potrf_diag_kernel    unblocked upper Cholesky of one nb x nb diagonal block, in smem
-//   potrf_panel_kernel   R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:]   (forward substitution)
+//   potrf_diag_kernel    upper Cholesky of one nb x nb diagonal block and its inverse, in smem
+//                        (the block row R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:] is then a GEMM)
 //   trtri_diag_kernel    inverses of the 64 x 64 diagonal blocks of R (blocked TRSM)
 //   shift_kernel         norm = Re tr(G) (= ||X||_F^2, reading #12); s = 11(mn+n(n+1)) u norm;
 //                        G += s I
@@ -31,6 +31,8 @@ __device__ __forceinline__ double2 s_add(double2 a, double2 b) { return make_dou
 __device__ __forceinline__ double s_add(double a, double b) { return a + b; }
 __device__ __forceinline__ double s_sub(double a, double b) { return a - b; }
 __device__ __forceinline__ double2 s_div(double2 a, double r) { return make_double2(a.x / r, a.y / r); }
+__device__ __forceinline__ double2 s_mulr(double2 a, double r) { return make_double2(a.x * r, a.y * r); }
+__device__ __forceinline__ double s_mulr(double a, double r) { return a * r; }
 __device__ __forceinline__ double s_div(double a, double r) { return a / r; }
 __device__ __forceinline__ double s_re(double2 a) { return a.x; }
 __device__ __forceinline__ double s_re(double a) { return a; }
@@ -42,96 +44,100 @@ __device__ __forceinline__ double s_abs2(double2 a) { return a.x * a.x + a.y * a
 __device__ __forceinline__ double s_abs2(double a) { return a * a; }
 __device__ __forceinline__ void s_add_re(double& a, double v) { a += v; }
 
-// One CTA.  G column-major (ld), block rows/cols [kb, kb+nb).  On exit the upper triangle of
-// the block holds R_kk (real positive diagonal).  Unblocked right-looking Cholesky in smem.
+// One CTA of POTRF_DIAG_THREADS.  G column-major (ld), block rows/cols [kb, kb+nb), nb <= 64.
+// On exit the upper triangle of the block holds R_kk (real positive diagonal) and, when Rinv is
+// not null, Rinv[0:nb, 0:nb] (ld 64) holds R_kk^{-1} (upper, zeros below), from which the block
+// row R[kb, kb+nb:] = R_kk^{-H} G[kb, kb+nb:] is one tensor-core GEMM (chase.cu, cholqr_pass).
+//  * factorisation: right-looking, column j at a time; the trailing update of the upper triangle
+//    is spread evenly over all threads through a table of the (a, b) pairs, a <= b, ordered by a
+//    descending, so step j updates exactly the first (nb-1-j)(nb-j)/2 entries;
+//  * inverse: recursive doubling in smem -- X_ii = 1/R_ii, then for w = 1, 2, .., 32 every
+//    pair of inverted w-blocks becomes a 2w-block, X12 = -X11 (R12 X22).
+// A non-positive (or NaN) pivot writes the 1-based global pivot into *info and returns.
+constexpr int POTRF_DIAG_THREADS = 256;
 template <typename T>
-constexpr int diag_smem() { return QR_NB * (QR_NB + 1) * (int)sizeof(T); }
+constexpr int diag_smem() { return 3 * QR_NB * (QR_NB + 1) * (int)sizeof(T) + QR_NB * (QR_NB + 1) / 2 * 2; }
 template <typename T>
-__global__ void potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info) {
+__global__ void __launch_bounds__(POTRF_DIAG_THREADS)
+    potrf_diag_kernel(T* G, long long ld, int kb, int nb, int* info, T* Rinv) {
   extern __shared__ __align__(16) unsigned char qr_dyn[];
-  T (*S)[QR_NB + 1] = reinterpret_cast<T (*)[QR_NB + 1]>(qr_dyn);   // S[a][b] = G[kb+a, kb+b]
+  constexpr int LD = QR_NB + 1;
+  T (*S)[LD] = reinterpret_cast<T (*)[LD]>(qr_dyn);                              // R
+  T (*X)[LD] = reinterpret_cast<T (*)[LD]>(qr_dyn + QR_NB * LD * sizeof(T));     // R^{-1}
+  T (*W)[LD] = reinterpret_cast<T (*)[LD]>(qr_dyn + 2 * QR_NB * LD * sizeof(T)); // temp
+  unsigned short* tab = reinterpret_cast<unsigned short*>(qr_dyn + 3 * QR_NB * LD * sizeof(T));
   if (*info != 0) return;
-  // 256 threads: thread (ty, b) owns column b = tid % 64 and rows ty, ty+4, ... of it
-  const int tid = threadIdx.x, b = tid & (QR_NB - 1), ty = tid >> 6;
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {   // coalesced: rows fastest
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < nb * nb; idx += POTRF_DIAG_THREADS) {   // coalesced: rows fastest
     const int a = idx % nb, c = idx / nb;
     S[a][c] = G[(long long)(kb + a) + (long long)(kb + c) * ld];
   }
+  // pair table: entry e <-> (a, b), a <= b < nb, a descending: pairs with a = nb-1-q start at
+  // q(q+1)/2; thread-parallel fill
+  const int npairs = nb * (nb + 1) / 2;
+  for (int e = tid; e < npairs; e += POTRF_DIAG_THREADS) {
+    int q = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);                  // largest q, q(q+1)/2 <= e
+    while ((q + 1) * (q + 2) / 2 <= e) ++q;
+    while (q * (q + 1) / 2 > e) --q;
+    const int a = nb - 1 - q, b = a + (e - q * (q + 1) / 2);
+    tab[e] = (unsigned short)((a << 8) | b);
+  }
   __syncthreads();
-  double rdiag = 0.0;                       // R[b][b], kept by the threads of column b
   for (int j = 0; j < nb; ++j) {
     const double d = s_re(S[j][j]);
     if (!(d > 0.0)) {                       // uniform: every thread reads the same d
       if (tid == 0) atomicCAS(info, 0, kb + j + 1);
       return;
     }
-    const double r = sqrt(d);
-    if (b == j) rdiag = r;
-    if (ty == 0 && b > j && b < nb) S[j][b] = s_div(S[j][b], r);   // row j of R
+    const double rinv = 1.0 / sqrt(d);
+    __syncthreads();                        // S[j][j] read by all before row j is scaled
+    if (tid >= j && tid < nb) S[j][tid] = tid == j ? s_real<T>(d * rinv) : s_mulr(S[j][tid], rinv);
     __syncthreads();
-    // trailing update of the upper triangle: S[a][b] -= conj(R[j][a]) R[j][b], j < a <= b
-    if (b > j && b < nb) {
-      const T rjb = S[j][b];
-      for (int a = j + 1 + ty; a <= b; a += 4) S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], rjb));
+    // S[a][b] -= conj(R[j][a]) R[j][b] for j < a <= b < nb: the first cnt table entries
+    const int cnt = (nb - 1 - j) * (nb - j) / 2;
+    for (int e = tid; e < cnt; e += POTRF_DIAG_THREADS) {
+      const int a = tab[e] >> 8, b = tab[e] & 255;
+      S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], S[j][b]));
     }
     __syncthreads();
   }
-  if (ty == 0 && b < nb) S[b][b] = s_real<T>(rdiag);
-  __syncthreads();
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {   // coalesced store of the upper part
+  for (int idx = tid; idx < nb * nb; idx += POTRF_DIAG_THREADS) {   // coalesced store (upper)
     const int a = idx % nb, c = idx / nb;
     if (a <= c) G[(long long)(kb + a) + (long long)(kb + c) * ld] = S[a][c];
   }
-}
-
-// R_kk^H Y = G[kb:kb+nb, kb+nb:n]: one thread per column, R_kk broadcast from smem, the column
-// kept in smem laid out [row][thread] (conflict free).
-constexpr int PANEL_THREADS = 64;    // columns per CTA (one solving thread each)
-constexpr int PANEL_BLOCK = 256;     // threads per CTA for the coalesced loads/stores
-template <typename T>
-constexpr int panel_smem() { return (QR_NB * QR_NB + QR_NB * PANEL_THREADS) * (int)sizeof(T); }
-template <typename T>
-__global__ void __launch_bounds__(PANEL_BLOCK)
-    potrf_panel_kernel(T* G, long long ld, int kb, int nb, int n, const int* info) {
-  extern __shared__ __align__(16) unsigned char qr_dyn[];
-  T (*R)[QR_NB] = reinterpret_cast<T (*)[QR_NB]>(qr_dyn);
-  T (*Y)[PANEL_THREADS] = reinterpret_cast<T (*)[PANEL_THREADS]>(qr_dyn + QR_NB * QR_NB * sizeof(T));
-  if (*info != 0) return;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < nb * nb; idx += PANEL_BLOCK) {
-    const int a = idx % nb, b = idx / nb;
-    R[a][b] = G[(long long)(kb + a) + (long long)(kb + b) * ld];
-  }
-  const int col0 = kb + nb + blockIdx.x * PANEL_THREADS;
-  const int col = col0 + tid;
-  const bool active = col < n;
-  // coalesced load of the nb x PANEL_THREADS panel by all PANEL_BLOCK threads (rows fastest)
-  for (int idx = tid; idx < nb * PANEL_THREADS; idx += PANEL_BLOCK) {
-    const int a = idx % nb, c = idx / nb;
-    if (col0 + c < n) Y[a][c] = G[(long long)(kb + a) + (long long)(col0 + c) * ld];
+  if (Rinv == nullptr) return;
+  // inverse by recursive doubling
+  for (int idx = tid; idx < QR_NB * QR_NB; idx += POTRF_DIAG_THREADS) {
+    const int a = idx % QR_NB, c = idx / QR_NB;
+    X[a][c] = (a == c && a < nb) ? s_real<T>(1.0 / s_re(S[a][a])) : s_real<T>(0.0);
   }
   __syncthreads();
-  if (tid < PANEL_THREADS) {
-  for (int a = 0; a < nb; ++a) {
-    // (R^H)[a][b] = conj(R[b][a]); four partial sums break the dependency chain
-    T acc0 = Y[a][tid], acc1 = s_real<T>(0.0), acc2 = s_real<T>(0.0), acc3 = s_real<T>(0.0);
-    int b = 0;
-    for (; b + 3 < a; b += 4) {
-      acc0 = s_sub(acc0, s_cmul(R[b][a], Y[b][tid]));
-      acc1 = s_sub(acc1, s_cmul(R[b + 1][a], Y[b + 1][tid]));
-      acc2 = s_sub(acc2, s_cmul(R[b + 2][a], Y[b + 2][tid]));
-      acc3 = s_sub(acc3, s_cmul(R[b + 3][a], Y[b + 3][tid]));
+  for (int w = 1; w < nb; w *= 2) {
+    // W[i0:j0, j0:j0+w2] = R12 X22 for every pair (i0 = 2 w p, j0 = i0 + w, w2 = min(w, nb - j0))
+    const int npair = (nb - w + 2 * w - 1) / (2 * w);
+    for (int e = tid; e < npair * w * w; e += POTRF_DIAG_THREADS) {
+      const int p = e / (w * w), r = (e % (w * w)) % w, c = (e % (w * w)) / w;
+      const int i0 = 2 * w * p, j0 = i0 + w;
+      if (j0 + c >= nb) continue;
+      T acc = s_real<T>(0.0);
+      for (int k = 0; k <= c; ++k) acc = s_add(acc, s_mul(S[i0 + r][j0 + k], X[j0 + k][j0 + c]));
+      W[i0 + r][j0 + c] = acc;
     }
-    for (; b < a; ++b) acc0 = s_sub(acc0, s_cmul(R[b][a], Y[b][tid]));
-    T acc = s_add(s_add(acc0, acc1), s_add(acc2, acc3));
-    acc = s_div(acc, s_re(R[a][a]));
-    if (active) Y[a][tid] = acc;
+    __syncthreads();
+    // X12 = -X11 W (X11 upper: k from r)
+    for (int e = tid; e < npair * w * w; e += POTRF_DIAG_THREADS) {
+      const int p = e / (w * w), r = (e % (w * w)) % w, c = (e % (w * w)) / w;
+      const int i0 = 2 * w * p, j0 = i0 + w;
+      if (j0 + c >= nb) continue;
+      T acc = s_real<T>(0.0);
+      for (int k = r; k < w; ++k) acc = s_add(acc, s_mul(X[i0 + r][i0 + k], W[i0 + k][j0 + c]));
+      X[i0 + r][j0 + c] = s_sub(s_real<T>(0.0), acc);
+    }
+    __syncthreads();
   }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nb * PANEL_THREADS; idx += PANEL_BLOCK) {
-    const int a = idx % nb, c = idx / nb;
-    if (col0 + c < n) G[(long long)(kb + a) + (long long)(col0 + c) * ld] = Y[a][c];
+  for (int idx = tid; idx < QR_NB * QR_NB; idx += POTRF_DIAG_THREADS) {
+    const int a = idx % QR_NB, c = idx / QR_NB;
+    Rinv[(long long)a + (long long)c * QR_NB] = (a < nb && c < nb && a <= c) ? X[a][c] : s_real<T>(0.0);
   }
 }
 
