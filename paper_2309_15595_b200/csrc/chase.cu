@@ -317,7 +317,7 @@ static bool g_disable_a3d = getenv("CHASE_DISABLE_A3D") != nullptr;   // A/B swi
 // (dynamic shared memory sizes of every variant are set once by preload_kernels)
 static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const ZGemmArgs& a, int grid_tiles = 0,
-                                   bool narrow = false, int nbatch = 1) {
+                                   bool narrow = false, int nbatch = 1, bool ext = false) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
   const int BN = narrow ? ZG_BN_NARROW : ZG_BN;
@@ -331,6 +331,10 @@ static chase_status_t launch_zgemm(chase_handle_s* h, bool conj, const CUtensorM
     return CHASE_OK;
   };
   constexpr int S = ZG_SMEM_BYTES, SN = zg_smem_bytes(ZG_BN_NARROW);
+  if (ext) {                                     // tri_k / batched (TRSM, TRTRI): NoTrans, plain
+    if (conj || split || narrow) return CHASE_EINVAL;
+    return go(zgemm_kernel<false, false, ZG_BN, true>, S);
+  }
   if (narrow) {
     if (conj) return split ? go(zgemm_kernel<true, true, ZG_BN_NARROW>, SN) : go(zgemm_kernel<true, false, ZG_BN_NARROW>, SN);
     return split ? go(zgemm_kernel<false, true, ZG_BN_NARROW>, SN) : go(zgemm_kernel<false, false, ZG_BN_NARROW>, SN);
@@ -345,7 +349,7 @@ static chase_status_t launch_zgemm_fused(chase_handle_s* h, bool conj, const CUt
 
 static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensorMap& tA,
                                    const CUtensorMap& tX, const DGemmArgs& a, int grid_tiles = 0,
-                                   bool narrow = false, int nbatch = 1) {
+                                   bool narrow = false, int nbatch = 1, bool ext = false) {
   if (a.M <= 0 || a.N <= 0) return CHASE_OK;
   const bool split = a.k_split > 1;
   const int BN = narrow ? DG_BN_NARROW : DG_BN;
@@ -359,6 +363,10 @@ static chase_status_t launch_dgemm(chase_handle_s* h, bool trans, const CUtensor
     return CHASE_OK;
   };
   constexpr int S = dg_smem_bytes(DG_BN), SN = dg_smem_bytes(DG_BN_NARROW);
+  if (ext) {                                     // tri_k / batched (TRSM, TRTRI): NoTrans, plain
+    if (trans || split || narrow) return CHASE_EINVAL;
+    return go(dgemm_kernel<false, false, DG_BN, true>, S);
+  }
   if (narrow) {
     if (trans) return split ? go(dgemm_kernel<true, true, DG_BN_NARROW>, SN) : go(dgemm_kernel<true, false, DG_BN_NARROW>, SN);
     return split ? go(dgemm_kernel<false, true, DG_BN_NARROW>, SN) : go(dgemm_kernel<false, false, DG_BN_NARROW>, SN);
@@ -417,7 +425,8 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
     a.col_shift = r.col_shift; a.y2 = static_cast<const double2*>(r.y2); a.ldy2 = r.ldy2;
     a.k_split = r.k_split; a.split_ld = r.split_ld;
     a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch);
+    return launch_zgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch,
+                        r.tri_k != 0 || r.nbatch > 1);
   }
   DGemmArgs a{};
   a.tri_k = r.tri_k;
@@ -435,7 +444,8 @@ static chase_status_t run_gemm(chase_handle_s* h, const GemmReq& r) {
   a.col_shift = r.col_shift; a.y2 = static_cast<const double*>(r.y2); a.ldy2 = r.ldy2;
   a.k_split = r.k_split; a.split_ld = r.split_ld;
   a.tail_tiles = r.tail_tiles; a.tile_offset = r.tile_offset;
-  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch);
+  return launch_dgemm(h, r.conj, *r.tA, *r.tX, a, r.grid_tiles, r.narrow != 0, r.nbatch,
+                      r.tri_k != 0 || r.nbatch > 1);
 }
 
 static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CUtensorMap& tA,
@@ -756,6 +766,8 @@ static chase_status_t preload_kernels() {
     ok &= smem((const void*)dgemm_kernel<false, false, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
     ok &= smem((const void*)dgemm_kernel<true, true, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
     ok &= smem((const void*)dgemm_kernel<false, true, DG_BN_NARROW>, dg_smem_bytes(DG_BN_NARROW));
+    ok &= smem((const void*)zgemm_kernel<false, false, ZG_BN, true>, ZG_SMEM_BYTES);
+    ok &= smem((const void*)dgemm_kernel<false, false, DG_BN, true>, dg_smem_bytes(DG_BN));
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);

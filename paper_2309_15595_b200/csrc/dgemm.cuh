@@ -91,7 +91,7 @@ __device__ __forceinline__ int dg_kperm(int t, int h) {
 // DG_BN for the bulk of a GEMM, DG_BN_NARROW for the N mod DG_BN remainder columns (a ragged
 // width pads to 32, not 128, columns; the ramp-degree steps of C5 wasted 3.8 % of their DMMA
 // work on padding with 128-wide tiles only).
-template <bool TRANS, bool SPLIT = false, int BN_ = DG_BN>
+template <bool TRANS, bool SPLIT = false, int BN_ = DG_BN, bool EXT = false>
 __global__ void __launch_bounds__(DG_THREADS, 1)
     dgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const DGemmArgs g) {
@@ -119,16 +119,16 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   const int gm = min(DG_GROUP_M, m_tiles - first_m);
   const int within = bid - group * DG_GROUP_M * n_tiles;
   const int m0 = (first_m + within % gm) * DG_BM;
-  const int n0 = (g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
+  const int n0 = (EXT && g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
   if (g.upper_only && m0 > n0 + BN_ - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int Kt = g.tri_k ? min(g.K, n0 + BN_) : g.K;      // K of this tile
+  const int Kt = EXT && g.tri_k ? min(g.K, n0 + BN_) : g.K;   // K of this tile
   const int KT_all = (Kt + DG_BKT - 1) / DG_BKT;
   const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * DG_BKT;
   const int Krem = Kt - kbase;                     // K left from this split's first k
-  const int bz = blockIdx.y;                       // batch index (0 unless batched)
+  const int bz = EXT ? (int)blockIdx.y : 0;       // batch index (EXT: batched launches)
   const int a_d0 = g.a_d0 + bz * g.bat_a, a_d1 = g.a_d1 + bz * g.bat_a;
   const int x_k0 = g.x_k0 + bz * g.bat_x, x_n0 = g.x_n0 + bz * g.bat_x;
   double* const gout = g.out + bz * g.bat_out;

@@ -93,8 +93,10 @@ struct ZGemmArgs {
 // SPLIT (compile time): split-K variant (k_split > 1); the default instantiation is the plain
 // GEMM with no split arithmetic in its hot loop.  BN_ (compile time): output columns per CTA --
 // ZG_BN for the bulk of a GEMM, ZG_BN_NARROW for the N mod ZG_BN remainder columns (so a
-// ragged width pads to 32, not 64, columns; the X tensor map box must match).
-template <bool CONJ, bool SPLIT = false, int BN_ = ZG_BN>
+// ragged width pads to 32, not 64, columns; the X tensor map box must match).  EXT (compile
+// time): the tri_k and batched modes of the TRSM / TRTRI; the filter instantiations leave them
+// out (their prologue arithmetic cost the filter HEMM 0.6 %, measured A/B on one box).
+template <bool CONJ, bool SPLIT = false, int BN_ = ZG_BN, bool EXT = false>
 __global__ void __launch_bounds__(ZG_THREADS, 1)
     zgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
                  const ZGemmArgs g) {
@@ -121,16 +123,16 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
   const int gm = min(ZG_GROUP_M, m_tiles - first_m);
   const int within = bid - group * ZG_GROUP_M * n_tiles;
   const int m0 = (first_m + within % gm) * ZG_BM;
-  const int n0 = (g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
+  const int n0 = (EXT && g.tri_k ? n_tiles - 1 - within / gm : within / gm) * BN_;
   if (g.upper_only && m0 > n0 + BN_ - 1) return;
   if (g.abort_flag != nullptr && *g.abort_flag != 0) return;
-  const int Kt = g.tri_k ? min(g.K, n0 + BN_) : g.K;      // K of this tile
+  const int Kt = EXT && g.tri_k ? min(g.K, n0 + BN_) : g.K;   // K of this tile
   const int KT_all = (Kt + ZG_BK - 1) / ZG_BK;
   const int KTc = SPLIT ? (KT_all + g.k_split - 1) / g.k_split : KT_all;
   const int KT = min(KTc, KT_all - split * KTc);   // >= 1: the host never launches an empty split
   const int kbase = split * KTc * ZG_BK;
   const int Krem = Kt - kbase;                     // K left from this split's first k
-  const int bz = blockIdx.y;                       // batch index (0 unless batched)
+  const int bz = EXT ? (int)blockIdx.y : 0;       // batch index (EXT: batched launches)
   const int a_d0 = g.a_d0 + bz * g.bat_a, a_d1 = g.a_d1 + bz * g.bat_a;
   const int x_k0 = g.x_k0 + bz * g.bat_x, x_n0 = g.x_n0 + bz * g.bat_x;
   double2* const gout = g.out + bz * g.bat_out;
