@@ -70,13 +70,33 @@ __device__ bool hh_cta_partial(const double (&v)[NV], double* part, unsigned* ct
   return last;
 }
 
-// fixed-order sum over the CTA partials (last CTA only); resets the arrival counter
+// fixed-order sum over the CTA partials (last CTA only); resets the arrival counter.  All
+// threads take part: GR groups of threads sum interleaved subsets of the CTA partials (loads of
+// a group in flight together), then the GR group sums are added in fixed order.
 template <int NV>
 __device__ void hh_grid_total(const double* part, int nv, double* out, unsigned* ctr) {
-  for (int k = threadIdx.x; k < nv; k += HH_THREADS) {
+  constexpr int GR = NV >= HH_THREADS ? 1 : (HH_THREADS / NV > 8 ? 8 : HH_THREADS / NV);
+  __shared__ double gsum[GR][NV];
+  const int k = threadIdx.x % NV, grp = threadIdx.x / NV;
+  const int nb = (int)gridDim.x;
+  if (grp < GR && k < nv) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int b = grp;
+    for (; b + 3 * GR < nb; b += 4 * GR) {
+      a0 += __ldcg(part + (size_t)b * NV + k);
+      a1 += __ldcg(part + (size_t)(b + GR) * NV + k);
+      a2 += __ldcg(part + (size_t)(b + 2 * GR) * NV + k);
+      a3 += __ldcg(part + (size_t)(b + 3 * GR) * NV + k);
+    }
+    for (; b < nb; b += GR) a0 += __ldcg(part + (size_t)b * NV + k);
+    gsum[grp][k] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+  for (int kk = threadIdx.x; kk < nv; kk += HH_THREADS) {
     double x = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) x += __ldcg(part + (size_t)b * NV + k);
-    out[k] = x;
+#pragma unroll
+    for (int g = 0; g < GR; ++g) x += gsum[g][kk];
+    out[kk] = x;
   }
   if (threadIdx.x == 0) *ctr = 0;
 }
@@ -197,6 +217,182 @@ __global__ void __launch_bounds__(HH_THREADS)
     }
   }
   if (ch == 0 && hh_cta_partial<3>(v3, part_n, ctr_n)) hh_grid_total<3>(part_n, 3, red_n, ctr_n);
+}
+
+// ---------------------------------------------------------------------------------------------
+// The whole panel [j0, pend) as ONE persistent kernel (column communicator of one member, p == 1):
+// the per-column steps of hh_norm / hh_reflect / hh_update with grid-wide barriers instead of
+// kernel boundaries (3 per column instead of 2 launches with a last-CTA reduction each).
+// Cooperative launch (all CTAs co-resident); CTA b owns the virtual rows
+// [b R, (b+1) R), R = ceil(n_r / gridDim.x).  Per column j:
+//   (a) every CTA sums the G partials of (||x_{>j}||^2, alpha) in fixed order -> xLARFG
+//       reflector (identical in every CTA); v_j into Vp[:, jj]; CTA partials of w = v_j^H X_panel
+//   (b) barrier; CTA b totals w for the columns c = b, b + G, ... (fixed order) -> wtot
+//   (c) barrier; X_panel -= conj(tau) v_j w on own rows, partials of column j+1's (norm, alpha)
+//   (d) barrier
+// Deterministic (fixed-order sums), identical to the launch-per-column path up to summation
+// order.  Workspace: part (G x (1 + nb) x 2 words ... see hhqr.inc), wtot (nb words), bar (2 u32).
+__device__ __forceinline__ void hh_grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = gen + 1;
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicExch(&bar[1], target);
+    } else {
+      while (*(volatile unsigned*)&bar[1] != target) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(HH_THREADS)
+    hh_panel_kernel(T* X, long long ldx, int n_r, long long voff, int j0, int pend, T* Vp,
+                    long long ldvp, T* tau_out, double* beta_out, double* part, T* wtot,
+                    unsigned* bar) {
+  constexpr int W = s_words<T>();
+  constexpr int NWARP = HH_THREADS / 32;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = (n_r + G - 1) / G, r0 = b * R, r1 = min(n_r, r0 + R);
+  const int nb = pend - j0;
+  // part layout: [0, 3G): (norm, alpha) partials; [3G, 3G + G nb W): w partials (CTA-major)
+  double* pn = part;
+  double* pw = part + 3 * G;
+  __shared__ double red[NWARP][HH_CH * 2];
+  __shared__ T sw[HH_NB];
+  unsigned gen = *(volatile unsigned*)&bar[1];
+  // CTA sum of a per-thread value set (nv <= 2 HH_CH doubles), fixed order.  Within a warp a
+  // reduce-scatter butterfly over 32 values (31 shuffles instead of 160): after step o, lane l
+  // keeps the partial sums of the values whose index agrees with l in the bits already folded;
+  // at the end lane l holds the warp total of value l.  Then the warps in order 0..7.
+  auto cta_sum = [&](double* v, int nv, double* dst) {
+    for (int base = 0; base < nv; base += 32) {
+      double x[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) x[k] = base + k < nv ? v[base + k] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          // keep x[k] (values with bit o clear) or x[k + o] (bit o set); send the other
+          const double send = up ? x[k] : x[k + o];
+          const double keep = up ? x[k + o] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (base + lane < nv) red[warp][base + lane] = x[0];
+    }
+    __syncthreads();
+    for (int k = tid; k < nv; k += HH_THREADS) {
+      double x = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) x += red[w][k];
+      dst[k] = x;
+    }
+    __syncthreads();
+  };
+  // initial (norm, alpha) partials of column j0
+  {
+    double v3[3] = {0.0, 0.0, 0.0};
+    for (int l = r0 + tid; l < r1; l += HH_THREADS) {
+      const long long g = voff + l;
+      const T x = X[(long long)l + (long long)j0 * ldx];
+      if (g > j0) v3[0] += s_abs2(x);
+      else if (g == j0) { v3[1] = s_re(x); v3[2] = s_im(x); }
+    }
+    cta_sum(v3, 3, pn + 3 * b);
+  }
+  hh_grid_barrier(bar, gen);
+  for (int jj = 0; jj < nb; ++jj) {
+    const int j = j0 + jj, nw = pend - j - 1;
+    // (a) reflector from the fixed-order total of the partials (same in every CTA)
+    double tot[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 3; ++k)
+      for (int bb = 0; bb < G; ++bb) tot[k] += __ldcg(pn + 3 * bb + k);
+    double beta;
+    T tau, inv;
+    hh_reflector<T>(tot, &beta, &tau, &inv);
+    if (b == 0 && tid == 0) {
+      tau_out[j] = tau;
+      beta_out[j] = beta;
+    }
+    // v_j on own rows; w partials in chunks of HH_CH columns
+    for (int c0 = 0; c0 < nw; c0 += HH_CH) {
+      const int nc = min(HH_CH, nw - c0);
+      T acc[HH_CH];
+#pragma unroll
+      for (int c = 0; c < HH_CH; ++c) acc[c] = s_real<T>(0.0);
+      for (int l = r0 + tid; l < r1; l += HH_THREADS) {
+        const long long g = voff + l;
+        if (g < j) {
+          if (c0 == 0) Vp[(long long)l + (long long)jj * ldvp] = s_real<T>(0.0);
+          continue;
+        }
+        const T v = g == j ? s_real<T>(1.0) : s_mul(X[(long long)l + (long long)j * ldx], inv);
+        if (c0 == 0) Vp[(long long)l + (long long)jj * ldvp] = v;
+#pragma unroll
+        for (int c = 0; c < HH_CH; ++c)
+          if (c < nc) acc[c] = s_add(acc[c], s_cmul(v, X[(long long)l + (long long)(j + 1 + c0 + c) * ldx]));
+      }
+      double vals[HH_CH * W];
+#pragma unroll
+      for (int c = 0; c < HH_CH; ++c) s_put(vals + c * W, acc[c]);
+      cta_sum(vals, nc * W, pw + ((size_t)b * HH_NB + c0) * W);
+    }
+    if (nw <= 0) {   // last column of the panel: v_j only
+      for (int l = r0 + tid; l < r1; l += HH_THREADS) {
+        const long long g = voff + l;
+        const T v = g < j ? s_real<T>(0.0) : (g == j ? s_real<T>(1.0) : s_mul(X[(long long)l + (long long)j * ldx], inv));
+        Vp[(long long)l + (long long)jj * ldvp] = v;
+      }
+      break;
+    }
+    hh_grid_barrier(bar, gen);
+    // (b) w totals, columns c = b, b + G, ... (fixed order over the CTAs)
+    for (int c = b + tid * G; c < nw; c += HH_THREADS * G) {
+      double x[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) x[k] = 0.0;
+      for (int bb = 0; bb < G; ++bb)
+#pragma unroll
+        for (int k = 0; k < W; ++k) x[k] += __ldcg(pw + ((size_t)bb * HH_NB + c) * W + k);
+      double* dst = reinterpret_cast<double*>(wtot + c);
+#pragma unroll
+      for (int k = 0; k < W; ++k) dst[k] = x[k];
+    }
+    hh_grid_barrier(bar, gen);
+    // (c) X_panel -= conj(tau) v w on own rows; (norm, alpha) partials of column j + 1
+    for (int c = tid; c < nw; c += HH_THREADS) sw[c] = s_mul(s_conj(tau), __ldcg(wtot + c));
+    __syncthreads();
+    double v3[3] = {0.0, 0.0, 0.0};
+    for (int l = r0 + tid; l < r1; l += HH_THREADS) {
+      const long long g = voff + l;
+      if (g < j) continue;
+      const T v = Vp[(long long)l + (long long)jj * ldvp];
+      T* row = X + (long long)l + (long long)(j + 1) * ldx;
+      for (int c0 = 0; c0 < nw; c0 += HH_CH) {
+        T xv[HH_CH];
+#pragma unroll
+        for (int c = 0; c < HH_CH; ++c)
+          if (c0 + c < nw) xv[c] = row[(long long)(c0 + c) * ldx];
+#pragma unroll
+        for (int c = 0; c < HH_CH; ++c)
+          if (c0 + c < nw) row[(long long)(c0 + c) * ldx] = xv[c] = s_sub(xv[c], s_mul(v, sw[c0 + c]));
+        if (c0 == 0) {
+          if (g > j + 1) v3[0] += s_abs2(xv[0]);
+          else if (g == j + 1) { v3[1] = s_re(xv[0]); v3[2] = s_im(xv[0]); }
+        }
+      }
+    }
+    cta_sum(v3, 3, pn + 3 * b);
+    hh_grid_barrier(bar, gen);
+  }
 }
 
 // After a panel: X[:, j0:pend] <- the LAPACK storage (v_j strictly below the pivot, beta_j on it)
