@@ -558,15 +558,22 @@ def main():
     if not args.no_extras:
         # ---- NEXT-2: Rayleigh-Ritz (Alg.2 l.16-22) on the step's orthonormal output, timed once
         cx.barrier()
+        cb.chase_profile_enable(P.h.h, True)
+        cb.chase_profile_read(P.h.h)
         e0.record(stream)
-        ritz, rr_sweeps = P.h.rayleigh_ritz(P.A_local, P.V)
+        ritz, rr_levels = P.h.rayleigh_ritz(P.A_local, P.V)
         e1.record(stream)
         cx.barrier()
+        rr_prof, _ = cb.chase_profile_read(P.h.h)
+        cb.chase_profile_enable(P.h.h, False)
         lam_sorted = np.sort(P.lam)
         extras["rayleigh_ritz"] = {
-            "ms": cx.allmax(e0.elapsed_time(e1)), "jacobi_sweeps": rr_sweeps,
+            "ms": cx.allmax(e0.elapsed_time(e1)), "eigensolver_ms": cx.allmax(rr_prof["other"]),
+            "hemm_ms": cx.allmax(rr_prof["hemm"]), "dc_levels": rr_levels,
             "max_ritz_minus_eig_lowest_nev": float(np.max(ritz[:w["nev"]] - lam_sorted[:w["nev"]])),
-            "note": "chase_rayleigh_ritz on the step output (NEXT-2, own block-Jacobi HEEVD), not part of the step"}
+            "note": "chase_rayleigh_ritz on the step output (NEXT-2): B = H C (one HEMM), the quotient, "
+                    "own HEEVD (Householder tridiagonalisation + divide and conquer + back-transform), "
+                    "V <- V Y; not part of the step"}
         # ---- NEXT-1: residual norms (Alg.2 l.23-28) of the Ritz pairs, timed separately
         P.h.residuals(P.A_local, P.V, ritz)                     # warm-up
         cx.barrier()

@@ -340,11 +340,15 @@ chase_status_t chase_solve(chase_handle_t h, const void* A_local, int64_t lda, v
  * Rayleigh-Ritz -- Alg.2 l.16-22 on the orthonormal
  * C-layout block V (ncols columns, e.g. the chase_cholqr output):
  *   B2 <- Bcast(C2, ccomm); B <- H C (odd-step HEMM), AllReduce(ccomm);
- *   A <- B2^H B, AllReduce(rcomm);  Lambda, Y <- HEEVD(A)  (own GPU parallel block-Jacobi
- *   eigensolver, redundant and bit-identical on every rank);  V <- V Y.
+ *   A <- B2^H B, AllReduce(rcomm);  Lambda, Y <- HEEVD(A)  (own GPU eigensolver: Householder
+ *   tridiagonalisation, Cuppen divide and conquer with Gu-Eisenstat eigenvectors, blocked
+ *   back-transformation; redundant and bit-identical on every rank; CHASE_RR_JACOBI=1 selects the
+ *   parallel block-Jacobi solver instead);  V <- V Y.
  *  ritz    host out: the ncols Ritz values, ascending (V's columns in the same order).
- *  sweeps  host out, nullable: Jacobi sweeps used (convergence: off(A) <= 1e-14 ||A||_F).
- * Uses the B-layout, Gram and eigensolver workspace.  Synchronises the stream once per sweep.
+ *  sweeps  host out, nullable: divide-and-conquer merge levels + 1 (Jacobi: sweeps used,
+ *          convergence off(A) <= 1e-14 ||A||_F).
+ * Uses the B-layout, Gram and eigensolver workspace.  Synchronises the stream once per merge
+ * level (host deflation decisions) or once per Jacobi sweep.
  * Errors: CHASE_EINVAL, CHASE_ESTATE, CHASE_ECUDA, CHASE_ENCCL, CHASE_ENOCONV (the Jacobi
  * solver did not reach its off-norm test within 40 sweeps; the results are written anyway). */
 chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_t lda, void* V,

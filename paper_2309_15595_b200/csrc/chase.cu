@@ -21,6 +21,7 @@
 #include "hhqr.cuh"
 #include "gemm_tail.cuh"
 #include "qr_kernels.cuh"
+#include "tridiag.cuh"
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
 #include "dgemm_fused.cuh"
@@ -238,7 +239,8 @@ static size_t eig_bytes(int64_t n_max) {
   const int64_t np = eig_np(n_max), L = np / 32;
   return 5 * align256((size_t)np * np * 16) + align256(np * sizeof(double)) +
          align256(np * sizeof(int)) + align256((size_t)(L + 1) * L * sizeof(int)) +
-         align256(2 * JAC_RED_BLOCKS * sizeof(double) + 2 * sizeof(double));
+         align256(2 * JAC_RED_BLOCKS * sizeof(double) + 2 * sizeof(double)) +
+         align256((size_t)(2 * 128 * np + 2 * 128 * 128) * 16);   // tridiagonal back-transform
 }
 // Householder QR scratch: panel reflectors Vp (n_r x 128), the compact-WY factors T of every
 // panel (128 x n_max), two 128 x n_max products, S = Vp^H Vp, tau, beta, CTA partials, split-K
@@ -1674,6 +1676,7 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
 bool g_qr_attr_done = false;
 
 #include "hhqr.inc"
+#include "heevd.inc"
 
 }  // namespace
 
@@ -1960,6 +1963,8 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
   tail += align256((size_t)(L + 1) * L * sizeof(int));
   double* d_part = reinterpret_cast<double*>(tail);
   double* d_off = d_part + 2 * JAC_RED_BLOCKS;
+  tail += align256(2 * JAC_RED_BLOCKS * sizeof(double) + 2 * sizeof(double));
+  double2* bt_tmp = reinterpret_cast<double2*>(tail);      // tridiagonal back-transform products
   STATUS_TRY(make_role_map(h, &tB2, y2, n_c, n, ldy2, ROLE_A_TRANS));
   STATUS_TRY(make_role_map(h, &tB, Bc, n_c, n, ldb, ROLE_X));
   const int64_t ldq = pad_ld(n);                       // real quotient / sorted Y in the G region
@@ -1979,6 +1984,48 @@ chase_status_t chase_rayleigh_ritz(chase_handle_t h, const void* A_local, int64_
   if (!cplx)
     real_to_complex_kernel<<<(unsigned)(((int64_t)n * n + TB - 1) / TB), TB, 0, h->stream>>>(
         static_cast<const double*>(h->Gws), ldq, Abuf[0], np, n);
+  // l.20 HEEVD.  Default: Householder tridiagonalisation + divide and conquer + back-transform
+  // (tridiag.cuh / heevd.inc); CHASE_RR_JACOBI=1: the parallel block-Jacobi solver below.
+  static const bool use_jacobi = getenv("CHASE_RR_JACOBI") != nullptr;
+  if (!use_jacobi) {
+    ProfScope ps_eig(h, CAT_OTHER, 0);
+    HeevdScratch hs{Abuf[1], np, reinterpret_cast<double*>(Ybuf[1]), reinterpret_cast<double*>(Ubd),
+                    (size_t)np * np * 2, bt_tmp};
+    std::vector<double> w;
+    int levels = 0;
+    STATUS_TRY(heevd_tridiag(h, Abuf[0], np, n, Ybuf[0], np, w, hs, &levels));
+    std::vector<int> cols(n);
+    for (int k = 0; k < n; ++k) cols[k] = k;
+    std::stable_sort(cols.begin(), cols.end(), [&](int a, int b) { return w[a] < w[b]; });
+    for (int k = 0; k < n; ++k) ritz[k] = w[cols[k]];
+    CUDA_TRY(cudaMemcpyAsync(d_order, cols.data(), n * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    const unsigned gn2 = (unsigned)(((int64_t)n * n + 255) / 256);
+    if (cplx)
+      jacobi_gather_kernel<double2><<<gn2, 256, 0, h->stream>>>(Ybuf[0], np, n, d_order,
+                                                                 static_cast<double2*>(h->Gws), ldq);
+    else
+      jacobi_gather_kernel<double><<<gn2, 256, 0, h->stream>>>(Ybuf[0], np, n, d_order,
+                                                                static_cast<double*>(h->Gws), ldq);
+    CUDA_TRY(cudaGetLastError());
+    CUtensorMap tV2, tY2;
+    int a3dV2 = 0;
+    STATUS_TRY(make_role_map(h, &tV2, V, n_r, n, ldv, ROLE_A_NOTRANS, &a3dV2));
+    STATUS_TRY(make_role_map(h, &tY2, h->Gws, n, n, ldq, ROLE_X));
+    char* W = static_cast<char*>(h->Wws);
+    const int64_t ldw = pad_ld(n_r);
+    {
+      GemmReq g{};
+      g.conj = false; g.tA = &tV2; g.tX = &tY2; g.a3d = a3dV2;
+      g.M = (int)n_r; g.N = n; g.K = n;
+      g.out = W; g.ldo = ldw; g.alpha = 1.0;
+      ProfScope ps(h, CAT_TRSM, 1);
+      STATUS_TRY(run_gemm(h, g));
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(V, ldv * es, W, ldw * es, n_r * es, n, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (sweeps_out) *sweeps_out = levels;
+    return CHASE_OK;
+  }
   jacobi_init_kernel<<<g2, TB, 0, h->stream>>>(Abuf[0], Ybuf[0], Ubd, np, n, (int)np, 0.0);
   CUDA_TRY(cudaGetLastError());
 
