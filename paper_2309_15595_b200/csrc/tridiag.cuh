@@ -153,6 +153,145 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- fused pipeline (two launches per column instead of three):
+//  trd_next_reflect_kernel(j): column j+1 of A22_j updated by step j's rank 2 (v_j, w_j), then the
+//     reflector of column j+1 from it (as trd_reflect_kernel), d[j+1] = Re A[j+1, j+1];
+//  trd_fused_kernel(j): the rest of step j's rank-2 update restricted to A22_{j+1} = A[j+2:, j+2:]
+//     (the only part read again), fused with step j+1's GEMV p' = tau' A22_{j+1} v' and w' -- one
+//     read and one write of the trailing matrix per column instead of two reads and one write.
+__global__ void __launch_bounds__(TRD_THREADS)
+    trd_next_reflect_kernel(const double2* A, long long lda, int n, int j, const double2* v,
+                            const double2* w, double2* Vst, long long ldv, double2* vnext,
+                            double2* tau, double* d, double* e) {
+  __shared__ double red[TRD_THREADS / 32];
+  __shared__ double2 head[2];
+  const int m = n - j - 1, tid = threadIdx.x;            // A22_j is m x m; next column = its col 0
+  const double2 w0 = w[0], v0 = v[0];
+  const double2 cw0 = make_double2(w0.x, -w0.y), cv0 = make_double2(v0.x, -v0.y);
+  const double2* col = A + (long long)(j + 1) + (long long)(j + 1) * lda;   // A22_j[:, 0]
+  auto upd = [&](int r) {                                 // updated A22_j[r, 0]
+    return s_sub(col[r], s_add(s_mul(v[r], cw0), s_mul(w[r], cv0)));
+  };
+  double s = 0.0;
+  for (int r = 2 + tid; r < m; r += TRD_THREADS) {
+    const double2 x = upd(r);
+    s += x.x * x.x + x.y * x.y;
+  }
+  if (tid == 0) {
+    head[0] = upd(0);
+    head[1] = m > 1 ? upd(1) : make_double2(0.0, 0.0);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((tid & 31) == 0) red[tid >> 5] = s;
+  __syncthreads();
+  double xn2 = 0.0;
+  for (int q = 0; q < TRD_THREADS / 32; ++q) xn2 += red[q];
+  const int jn = j + 1, mn = m - 1;                       // next column index, its length
+  const double ar = head[1].x, ai = head[1].y;
+  double beta;
+  double2 t, inv;
+  if (xn2 == 0.0 && ai == 0.0) {
+    beta = ar;
+    t = make_double2(0.0, 0.0);
+    inv = make_double2(1.0, 0.0);
+  } else {
+    beta = -copysign(sqrt(ar * ar + ai * ai + xn2), ar);
+    t = make_double2((beta - ar) / beta, -ai / beta);
+    const double dr = ar - beta, di = ai, den = dr * dr + di * di;
+    inv = make_double2(dr / den, -di / den);
+  }
+  for (int i = tid; i < mn; i += TRD_THREADS) {
+    const double2 vv = i == 0 ? make_double2(1.0, 0.0) : s_mul(upd(i + 1), inv);
+    vnext[i] = vv;
+    Vst[(long long)(jn + 1 + i) + (long long)jn * ldv] = vv;
+  }
+  if (tid == 0) {
+    tau[jn] = t;
+    d[jn] = head[0].x;
+    e[jn] = beta;
+  }
+}
+
+constexpr int TRD_FUSED_WARPS = 8;
+__global__ void __launch_bounds__(TRD_FUSED_WARPS * 32)
+    trd_fused_kernel(double2* A, long long lda, int n, int j, const double2* v, const double2* w,
+                     const double2* vn, const double2* tau, double2* pbuf, double2* wbuf,
+                     double* part, unsigned* ctr) {
+  const int m = n - j - 1, mn = m - 1, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double2 tn = tau[j + 1];
+  const int c = blockIdx.x * TRD_FUSED_WARPS + warp;     // column of A22_{j+1}
+  __shared__ double2 dots[TRD_FUSED_WARPS];
+  __shared__ bool last;
+  double2 dot = make_double2(0.0, 0.0);
+  if (c < mn) {
+    // A22_j[r, c+1] for r = 1..m-1  ->  A22_{j+1}[r-1, c]
+    double2* colp = A + (long long)(j + 2) + (long long)(j + 2 + c) * lda;
+    const double2 wc = w[c + 1], vc = v[c + 1];
+    const double2 cwc = make_double2(wc.x, -wc.y), cvc = make_double2(vc.x, -vc.y);
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+    int r = lane;
+    for (; r + 32 < mn; r += 64) {
+      const double2 x0 = colp[r], x1 = colp[r + 32];
+      const double2 y0 = s_sub(x0, s_add(s_mul(v[r + 1], cwc), s_mul(w[r + 1], cvc)));
+      const double2 y1 = s_sub(x1, s_add(s_mul(v[r + 33], cwc), s_mul(w[r + 33], cvc)));
+      colp[r] = y0;
+      colp[r + 32] = y1;
+      a0 = s_add(a0, s_cmul(y0, vn[r]));
+      a1 = s_add(a1, s_cmul(y1, vn[r + 32]));
+    }
+    for (; r < mn; r += 32) {
+      const double2 y = s_sub(colp[r], s_add(s_mul(v[r + 1], cwc), s_mul(w[r + 1], cvc)));
+      colp[r] = y;
+      a0 = s_add(a0, s_cmul(y, vn[r]));
+    }
+    double2 acc = s_add(a0, a1);
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    const double2 p = s_mul(tn, acc);
+    if (lane == 0) pbuf[c] = p;
+    dot = s_cmul(p, vn[c]);
+  }
+  if (lane == 0) dots[warp] = dot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = 0; q < TRD_FUSED_WARPS; ++q) s = s_add(s, dots[q]);
+    part[2 * blockIdx.x] = s.x;
+    part[2 * blockIdx.x + 1] = s.y;
+    __threadfence();
+    last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 tsum[TRD_FUSED_WARPS * 32];
+  __shared__ double2 alpha;
+  {
+    double2 s = make_double2(0.0, 0.0);
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      s = s_add(s, make_double2(__ldcg(part + 2 * b), __ldcg(part + 2 * b + 1)));
+    tsum[threadIdx.x] = s;
+  }
+  __syncthreads();
+  for (int q = TRD_FUSED_WARPS * 16; q > 0; q >>= 1) {
+    if ((int)threadIdx.x < q) tsum[threadIdx.x] = s_add(tsum[threadIdx.x], tsum[threadIdx.x + q]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double2 a = s_mul(tn, tsum[0]);
+    alpha = make_double2(-0.5 * a.x, -0.5 * a.y);
+    *ctr = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < mn; i += blockDim.x) wbuf[i] = s_add(__ldcg(pbuf + i), s_mul(alpha, vn[i]));
+}
+
+__global__ void trd_last_diag_kernel(const double2* A, long long lda, int n, double* d) {
+  d[n - 1] = A[(long long)(n - 1) + (long long)(n - 1) * lda].x;
+}
+
 // A <- (A + A^H) / 2 (the reduced quotient B2^H B is Hermitian only up to rounding)
 __global__ void trd_symmetrize_kernel(double2* A, long long lda, int n) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
