@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(TRD_THREADS)
 
 constexpr int TRD_FUSED_WARPS = 8;
 __global__ void __launch_bounds__(TRD_FUSED_WARPS * 32)
-    trd_fused_kernel(double2* A, long long lda, int n, int j, const double2* v, const double2* w,
-                     const double2* vn, const double2* tau, double2* pbuf, double2* wbuf,
-                     double* part, unsigned* ctr) {
+    trd_fused_kernel(double2* __restrict__ A, long long lda, int n, int j, const double2* __restrict__ v,
+                     const double2* __restrict__ w, const double2* __restrict__ vn, const double2* tau,
+                     double2* pbuf, double2* wbuf, double* part, unsigned* ctr) {
   const int m = n - j - 1, mn = m - 1, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double2 tn = tau[j + 1];
   const int c = blockIdx.x * TRD_FUSED_WARPS + warp;     // column of A22_{j+1}
@@ -225,19 +225,22 @@ __global__ void __launch_bounds__(TRD_FUSED_WARPS * 32)
   double2 dot = make_double2(0.0, 0.0);
   if (c < mn) {
     // A22_j[r, c+1] for r = 1..m-1  ->  A22_{j+1}[r-1, c]
-    double2* colp = A + (long long)(j + 2) + (long long)(j + 2 + c) * lda;
+    double2* __restrict__ colp = A + (long long)(j + 2) + (long long)(j + 2 + c) * lda;
     const double2 wc = w[c + 1], vc = v[c + 1];
     const double2 cwc = make_double2(wc.x, -wc.y), cvc = make_double2(vc.x, -vc.y);
     double2 a0 = make_double2(0.0, 0.0), a1 = a0;
     int r = lane;
-    for (; r + 32 < mn; r += 64) {
-      const double2 x0 = colp[r], x1 = colp[r + 32];
-      const double2 y0 = s_sub(x0, s_add(s_mul(v[r + 1], cwc), s_mul(w[r + 1], cvc)));
-      const double2 y1 = s_sub(x1, s_add(s_mul(v[r + 33], cwc), s_mul(w[r + 33], cvc)));
-      colp[r] = y0;
-      colp[r + 32] = y1;
-      a0 = s_add(a0, s_cmul(y0, vn[r]));
-      a1 = s_add(a1, s_cmul(y1, vn[r + 32]));
+    for (; r + 96 < mn; r += 128) {                       // 4 columns chunks, loads first
+      double2 x[4], y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = colp[r + 32 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        y[q] = s_sub(x[q], s_add(s_mul(v[r + 32 * q + 1], cwc), s_mul(w[r + 32 * q + 1], cvc)));
+        colp[r + 32 * q] = y[q];
+      }
+      a0 = s_add(a0, s_add(s_cmul(y[0], vn[r]), s_cmul(y[2], vn[r + 64])));
+      a1 = s_add(a1, s_add(s_cmul(y[1], vn[r + 32]), s_cmul(y[3], vn[r + 96])));
     }
     for (; r < mn; r += 32) {
       const double2 y = s_sub(colp[r], s_add(s_mul(v[r + 1], cwc), s_mul(w[r + 1], cvc)));
