@@ -48,12 +48,35 @@ __device__ bool hh_cta_partial(const double (&v)[NV], double* part, unsigned* ct
   __shared__ double wsum[HH_THREADS / 32][NV];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (NV % 32 == 0) {
+    // warp reduce-scatter butterfly per group of 32 values (31 shuffles instead of 160): after the
+    // step with mask o a lane keeps the partial sums of the values whose index agrees with the
+    // lane in bit o; lane l ends with the warp total of value l of the group
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double x = v[k];
+    for (int base = 0; base < NV; base += 32) {
+      double x[32];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) wsum[warp][k] = x;
+      for (int k = 0; k < 32; ++k) x[k] = v[base + k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+          const double send = up ? x[k] : x[k + o];
+          const double keep = up ? x[k + o] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      wsum[warp][base + lane] = x[0];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double x = v[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) wsum[warp][k] = x;
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < NV; k += HH_THREADS) {
