@@ -15,7 +15,10 @@
  *    unless stated otherwise.
  *  - The handle is not thread-safe; one handle per process/GPU.
  *  - Collective calls (chase_filter, chase_cholqr) must be made by every rank of the grid with
- *    identical scalar arguments (SPMD); otherwise the result is undefined or a hang.
+ *    identical scalar arguments (SPMD); otherwise the result is undefined or a hang.  With
+ *    CHASE_SPMD_CHECK=1 in the environment (or a -DCHASE_DEBUG build) they first compare a hash
+ *    of those arguments over the world communicator and return CHASE_EINVAL on every rank when
+ *    they differ (two tiny AllReduces and one stream synchronisation per call).
  *  - Argument errors are reported synchronously, before any device work, and leave all
  *    buffers untouched.
  */

@@ -668,6 +668,46 @@ static chase_status_t allreduce_cols(chase_handle_s* h, void* buf, int64_t rows,
   return CHASE_OK;
 }
 
+// ==================================================================== SPMD argument check
+// Collective calls need identical scalar arguments on every rank (include/chase.h).  With
+// CHASE_SPMD_CHECK=1 in the environment (or a -DCHASE_DEBUG build) the call hashes them (FNV-1a
+// over the raw bytes) and compares min and max of the hash over the world communicator; a
+// mismatch returns CHASE_EINVAL on every rank before any device work.  Costs two tiny
+// AllReduces and a stream synchronisation, so it is off by default.
+static bool spmd_check_enabled() {
+#ifdef CHASE_DEBUG
+  return true;
+#else
+  static const bool on = getenv("CHASE_SPMD_CHECK") != nullptr && atoi(getenv("CHASE_SPMD_CHECK")) != 0;
+  return on;
+#endif
+}
+struct SpmdHash {
+  uint64_t v = 1469598103934665603ull;
+  void add(const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) v = (v ^ b[i]) * 1099511628211ull;
+  }
+  template <typename T> void add(const T& x) { add(&x, sizeof(T)); }
+};
+static chase_status_t spmd_verify(chase_handle_s* h, uint64_t hash) {
+  if (!spmd_check_enabled() || h->world == nullptr) return CHASE_OK;
+  uint64_t* d = reinterpret_cast<uint64_t*>(h->d_shift) + 1;   // scratch words after the shift
+  uint64_t hv[2] = {hash, hash};
+  CUDA_TRY(cudaMemcpyAsync(d, hv, 16, cudaMemcpyHostToDevice, h->stream));
+  NCCL_TRY(ncclGroupStart());
+  NCCL_TRY(ncclAllReduce(d, d, 1, ncclUint64, ncclMin, h->world, h->stream));
+  NCCL_TRY(ncclAllReduce(d + 1, d + 1, 1, ncclUint64, ncclMax, h->world, h->stream));
+  NCCL_TRY(ncclGroupEnd());
+  CUDA_TRY(cudaMemcpyAsync(hv, d, 16, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (hv[0] != hv[1]) {
+    fprintf(stderr, "[chase] SPMD check: arguments differ across ranks\n");
+    return CHASE_EINVAL;
+  }
+  return CHASE_OK;
+}
+
 // ==================================================================== fused-comm workspace
 // Symmetric region (identical size and layout on every rank, peer-mapped by the caller):
 //   Cw  C-layout working block  pad(ceil(N/p)) x n_max      (filter even-step outputs)
@@ -1154,6 +1194,15 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
     return CHASE_EINVAL;
   if (((size_t)lda * es) % 16 || ((size_t)ldv * es) % 16) return CHASE_EINVAL;   // TMA pitch
 
+  if (spmd_check_enabled()) {
+    SpmdHash hs;
+    hs.add(ncols);
+    hs.add(degrees, (size_t)ncols * sizeof(int32_t));
+    hs.add(c);
+    hs.add(e);
+    hs.add(*bounds);
+    STATUS_TRY(spmd_verify(h, hs.v));
+  }
   std::vector<chase_step_record_t> rec;
   int64_t mv;
   build_schedule(Geom{h->n_r, h->n_c, h->r0, h->c0, h->myrow, h->mycol, h->nb}, ncols, degrees, &rec, &mv);
@@ -1699,6 +1748,13 @@ chase_status_t chase_cholqr(chase_handle_t h, void* V, int64_t ldv, int64_t ncol
     g_qr_attr_done = true;
   }
   const int n = (int)ncols;
+  if (spmd_check_enabled()) {
+    SpmdHash hs;
+    hs.add(ncols);
+    hs.add(cond_est);
+    hs.add(h->qr_mode);
+    STATUS_TRY(spmd_verify(h, hs.v));
+  }
   QrMaps mp;
   STATUS_TRY(make_role_map(h, &mp.vA_t, V, h->n_r, n, ldv, ROLE_A_TRANS));
   STATUS_TRY(make_role_map(h, &mp.vA_nt, V, h->n_r, n, ldv, ROLE_A_NOTRANS, &mp.v_a3d));

@@ -158,3 +158,17 @@ def test_solve_grid(tmp_path, grid):
     X = res["X"][:, :nev]
     rr = oracle.residuals(A, X, res["lam"][:nev])
     assert np.max(rr) <= 1e-9
+
+
+def test_spmd_check(tmp_path):
+    """include/chase.h: collective calls need identical scalar arguments; with CHASE_SPMD_CHECK=1
+    a disagreeing rank makes chase_filter return CHASE_EINVAL on every rank (hash min != max over
+    the world communicator) before any device work."""
+    import json
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = str(tmp_path / "spmd.json")
+    r = torchrun(2, [os.path.join(ROOT, "tests", "mp_spmd_worker.py"), out], 300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for res in json.load(open(out)):
+        assert res["mismatch_status"] == 1 and res["untouched"] and res["agree_status"] == 0, res
