@@ -1638,6 +1638,7 @@ chase_status_t cholqr_pass(chase_handle_s* h, void* V, int64_t ldv, int n, bool 
         g.a_d0 = i0; g.a_d1 = j0; g.x_k0 = j0; g.x_n0 = j0;
         g.out = Tmp + ((size_t)i0 + (size_t)j0 * ldf) * es; g.ldo = ldf; g.alpha = 1.0;
         g.nbatch = cnt; g.bat_a = st; g.bat_x = st; g.bat_out = (int64_t)st * (1 + ldf);
+        g.tri_k = 1;                          // R22^{-1} upper triangular: k < n0 + BN per tile
         STATUS_TRY(run_gemm(h, g));
         GemmReq g2{};                         // X12 = -R11^{-1} Tmp
         g2.conj = false; g2.tA = &mp.rfA_nt; g2.tX = &mp.tmpX;

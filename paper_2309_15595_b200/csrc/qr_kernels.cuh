@@ -83,24 +83,31 @@ __global__ void __launch_bounds__(POTRF_DIAG_THREADS)
     tab[e] = (unsigned short)((a << 8) | b);
   }
   __syncthreads();
+  // one barrier per column: row j is used unscaled (conj(R_ja) R_jb = conj(S_ja) S_jb / d_j) and
+  // scaled by 1/sqrt(d_j) only after the loop -- rows <= j are never written after step j
   for (int j = 0; j < nb; ++j) {
     const double d = s_re(S[j][j]);
     if (!(d > 0.0)) {                       // uniform: every thread reads the same d
       if (tid == 0) atomicCAS(info, 0, kb + j + 1);
       return;
     }
-    const double rinv = 1.0 / sqrt(d);
-    __syncthreads();                        // S[j][j] read by all before row j is scaled
-    if (tid >= j && tid < nb) S[j][tid] = tid == j ? s_real<T>(d * rinv) : s_mulr(S[j][tid], rinv);
-    __syncthreads();
-    // S[a][b] -= conj(R[j][a]) R[j][b] for j < a <= b < nb: the first cnt table entries
+    const double dinv = 1.0 / d;
+    // S[a][b] -= conj(S[j][a]) S[j][b] / d for j < a <= b < nb: the first cnt table entries
     const int cnt = (nb - 1 - j) * (nb - j) / 2;
     for (int e = tid; e < cnt; e += POTRF_DIAG_THREADS) {
       const int a = tab[e] >> 8, b = tab[e] & 255;
-      S[a][b] = s_sub(S[a][b], s_cmul(S[j][a], S[j][b]));
+      S[a][b] = s_sub(S[a][b], s_mulr(s_cmul(S[j][a], S[j][b]), dinv));
     }
     __syncthreads();
   }
+  // R[j][j] = sqrt(d_j), R[j][b] = S[j][b] / sqrt(d_j) (b > j)
+  for (int idx = tid; idx < nb * nb; idx += POTRF_DIAG_THREADS) {
+    const int a = idx % nb, c = idx / nb;
+    if (a < c) S[a][c] = s_mulr(S[a][c], 1.0 / sqrt(s_re(S[a][a])));
+  }
+  __syncthreads();
+  for (int a = tid; a < nb; a += POTRF_DIAG_THREADS) S[a][a] = s_real<T>(sqrt(s_re(S[a][a])));
+  __syncthreads();
   for (int idx = tid; idx < nb * nb; idx += POTRF_DIAG_THREADS) {   // coalesced store (upper)
     const int a = idx % nb, c = idx / nb;
     if (a <= c) G[(long long)(kb + a) + (long long)(kb + c) * ld] = S[a][c];
