@@ -191,11 +191,15 @@ __global__ void __launch_bounds__(HH_THREADS)
       if (ch == 0) vpc[l] = s_real<T>(0.0);
       continue;
     }
+    T xv[HH_CH];
+#pragma unroll
+    for (int c = 0; c < HH_CH; ++c)
+      if (c < nc) xv[c] = X[(long long)l + (long long)(c0 + c) * ldx];
     const T v = g == j ? s_real<T>(1.0) : s_mul(colj[l], inv);
     if (ch == 0) vpc[l] = v;
 #pragma unroll
     for (int c = 0; c < HH_CH; ++c)
-      if (c < nc) acc[c] = s_add(acc[c], s_cmul(v, X[(long long)l + (long long)(c0 + c) * ldx]));
+      if (c < nc) acc[c] = s_add(acc[c], s_cmul(v, xv[c]));
   }
   if (nc <= 0) return;                                  // uniform over the CTA
   double vals[NV];
@@ -226,12 +230,16 @@ __global__ void __launch_bounds__(HH_THREADS)
     const long long g = voff + l;
     if (g < j) continue;
     const T v = vpc[l];
+    T* row = X + (long long)l + (long long)c0 * ldx;
+    T xv[HH_CH];
+#pragma unroll
+    for (int c = 0; c < HH_CH; ++c)          // all loads first (the stores below may alias them
+      if (c < nc) xv[c] = row[(long long)c * ldx];   // as far as the compiler knows)
 #pragma unroll
     for (int c = 0; c < HH_CH; ++c) {
       if (c < nc) {
-        T* p = X + (long long)l + (long long)(c0 + c) * ldx;
-        const T x = s_sub(*p, s_mul(v, w[c]));
-        *p = x;
+        const T x = s_sub(xv[c], s_mul(v, w[c]));
+        row[(long long)c * ldx] = x;
         if (ch == 0 && c == 0) {
           if (g > j + 1) v3[0] += s_abs2(x);
           else if (g == j + 1) { v3[1] = s_re(x); v3[2] = s_im(x); }
