@@ -3,8 +3,8 @@
 
 * fused self mode (chase_set_fused_mode(h, 1)): a 1x1 grid whose every filter step runs
   zgemm_fused_kernel / dgemm_fused_kernel through the push/owner/broadcast protocol with m = 1;
-* virtual grids (chase_create_virtual): all p*q ranks of a 2x1 / 1x2 / 2x2 / 1x4 grid (block
-  and block-cyclic) live in this process on one GPU, each on its own stream and host thread,
+* virtual grids (chase_create_virtual): all p*q ranks of a 2x1 / 1x2 / 2x2 / 1x4 / 2x4 grid
+  (block and block-cyclic; 2x4 is BASELINE's 8-GPU grid) live in this process on one GPU, each on its own stream and host thread,
   with their fused regions peer-mapped to each other (same device), so the fused kernels run
   their multi-member protocol (m = 2 and 4) -- results equal to the global oracle, replicas
   bitwise identical;
@@ -116,7 +116,7 @@ def run_virtual(A, V0, degs, b, p, q, nb, complex_, budget=None):
 
 @pytest.mark.parametrize("complex_", [True, False])
 @pytest.mark.parametrize("grid,nb", [((2, 1), 0), ((1, 2), 0), ((2, 2), 0), ((1, 4), 0), ((2, 2), 16),
-                                     ((2, 1), 7)])
+                                     ((2, 1), 7), ((2, 4), 0), ((2, 4), 9)])
 def test_virtual_grid_fused_matches_oracle(complex_, grid, nb):
     """Fused multi-member kernels (m = p on odd steps, m = q on even steps) on one GPU."""
     p, q = grid
