@@ -25,6 +25,7 @@
 #include "zgemm.cuh"
 #include "zgemm_fused.cuh"
 #include "dgemm_fused.cuh"
+#include "fused_tail.cuh"
 
 using namespace chase;
 
@@ -163,6 +164,7 @@ struct chase_handle_s {
   int world_size = 1;
   unsigned fused_ep = 0;
   unsigned long long fused_delivered = 0;
+  unsigned fused_tail_k[2] = {0, 0};  // fused odd / even steps so far: tail slot rotation
   int* d_err = nullptr;
   int num_sms = 148;
   // bookkeeping of the last filter call
@@ -475,6 +477,33 @@ static chase_status_t launch_dgemm_fused(chase_handle_s* h, bool trans, const CU
   return CHASE_OK;
 }
 
+// Wave-quantisation tail plan for T equal-cost tiles of KT k-tiles on G co-resident CTAs: the
+// last T_tail tiles as S split-K copies, (T_tail, S) minimising the modelled waves (T_tail = the
+// partial last wave, or it plus one full wave); S = 1: no split (nothing gained).  T_tail <= cap.
+static void plan_tail(int T, int KT, int G, int cap, int* S_out, int* tail_out) {
+  *S_out = 1;
+  *tail_out = 0;
+  const int full = T / G, rem = T % G;
+  if (rem == 0) return;
+  double best_gain = 0.02;                 // in waves; below this the split is not worth it
+  for (int extra = 0; extra <= std::min(1, full); ++extra) {
+    const int tail = rem + extra * G;
+    if (tail > cap) break;
+    for (int S = 2; S <= 8; ++S) {
+      if (KT < 2 * S || S * tail > TAIL_TILES_MAX) break;
+      const int ktc = (KT + S - 1) / S;
+      if ((KT + ktc - 1) / ktc != S) continue;   // S copies must all be non-empty
+      const double waves = (double)((S * tail + G - 1) / G) / S;
+      const double gain = (extra + 1) - waves;
+      if (gain > best_gain) {
+        best_gain = gain;
+        *S_out = S;
+        *tail_out = tail;
+      }
+    }
+  }
+}
+
 // A big GEMM with its wave-quantisation tail split over K (gemm_tail.cuh): the plain kernel on
 // the first T_main tiles of the raster, the last T_tail tiles as S split-K copies into tile-local
 // partials, then the fixed-order sum + epilogue.  (T_tail, S) minimise the modelled waves
@@ -516,25 +545,8 @@ static chase_status_t run_gemm_tail(chase_handle_s* h, const GemmReq& g) {
   const int BN = cplx ? (g.narrow ? ZG_BN_NARROW : ZG_BN) : (g.narrow ? DG_BN_NARROW : DG_BN);
   const int T = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int SMS = h->num_sms, KT = (g.K + BK - 1) / BK;
-  const int full = T / SMS, rem = T % SMS;
-  if (rem == 0) return run_gemm(h, g);
-  double best_gain = 0.02;                 // in waves; below this the split is not worth it
-  int bS = 1, btail = 0;
-  for (int extra = 0; extra <= std::min(1, full); ++extra) {
-    const int tail = rem + extra * SMS;
-    for (int S = 2; S <= 8; ++S) {
-      if (KT < 2 * S || S * tail > TAIL_TILES_MAX) break;
-      const int ktc = (KT + S - 1) / S;
-      if ((KT + ktc - 1) / ktc != S) continue;   // S copies must all be non-empty
-      const double waves = (double)((S * tail + SMS - 1) / SMS) / S;
-      const double gain = (extra + 1) - waves;
-      if (gain > best_gain) {
-        best_gain = gain;
-        bS = S;
-        btail = tail;
-      }
-    }
-  }
+  int bS, btail;
+  plan_tail(T, KT, SMS, TAIL_TILES_MAX, &bS, &btail);
   if (bS == 1) return run_gemm(h, g);
   const int tmain = T - btail;
   if (tmain > 0) {
@@ -714,10 +726,12 @@ static chase_status_t spmd_verify(chase_handle_s* h, uint64_t hash) {
 //   Bw  B-layout working block  pad(ceil(N/q)) x n_max      (filter odd-step outputs)
 //   P   partial tiles           pad(max rows)  x n_max
 //   flags [tile * m + src] u32  (tiles of the largest step) x max(p, q), one array per parity
-//   done  u64 delivery counter, err i32
+//   done  u64 delivery counter, err i32, tile-scheduler counter
+//   tailp FUSED_TAIL_SLOTS slots x max(p, q) sub-slots of split-K tail partial tiles,
+//         tflags [slot][src] (fused_tail.cuh)
 struct FusedLayout {
   int64_t ldc, ldb, ldpo, ldpe;
-  size_t cw, bw, po, pe, flags, done, err, ctr, total;
+  size_t cw, bw, po, pe, flags, done, err, ctr, tailp, tflags, total;
   int64_t tiles_max;
 };
 // Staging areas by step parity (odd steps: p slots of B-layout rows, even: q slots of C-layout
@@ -762,6 +776,10 @@ static FusedLayout fused_layout(const chase_handle_s* h) {
   off += 256;
   L.ctr = off;                                          // dynamic tile-scheduler counter
   off += 256;
+  L.tailp = off;                                        // split-K tail partials (fused_tail.cuh)
+  off += align256((size_t)FUSED_TAIL_SLOTS * std::max(h->p, h->q) * FUSED_TAIL_TILES * 128 * 128 * 8);
+  L.tflags = off;                                       // tail flags [slot][src]
+  off += align256((size_t)FUSED_TAIL_SLOTS * FUSED_MAX_MEMBERS * sizeof(unsigned));
   L.total = off;
   return L;
 }
@@ -814,6 +832,15 @@ static chase_status_t preload_kernels() {
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);
     ok &= smem((const void*)gemm_tail_epilogue_kernel<double, DG_BM, DG_BN, DG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_sync_kernel, 0);
+    ok &= smem((const void*)fused_tail_publish_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_publish_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_publish_kernel<double, DG_BM, DG_BN, DG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_publish_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_reduce_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_reduce_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_reduce_kernel<double, DG_BM, DG_BN, DG_GROUP_M>, 0);
+    ok &= smem((const void*)fused_tail_reduce_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M>, 0);
     if (!ok) {
       fprintf(stderr, "[chase] kernel preload failed: %s\n", cudaGetErrorString(cudaGetLastError()));
       status = CHASE_ECUDA;
@@ -1131,13 +1158,16 @@ chase_status_t chase_set_fused_workspace(chase_handle_t h, void* local, const ui
   }
   h->world_size = world;
   const FusedLayout L = fused_layout(h);
-  // flags, counter and error word start at zero; the caller barriers all ranks before use
-  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(local) + L.flags, 0, L.total - L.flags, h->stream));
+  // flags, counters, error word and tail flags start at zero; the caller barriers all ranks
+  // before use
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(local) + L.flags, 0, L.tailp - L.flags, h->stream));
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(local) + L.tflags, 0, L.total - L.tflags, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   CUDA_TRY(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->d_err = reinterpret_cast<int*>(static_cast<char*>(local) + L.err);
   h->fused_ep = 0;
   h->fused_delivered = 0;
+  h->fused_tail_k[0] = h->fused_tail_k[1] = 0;
   h->fused_broken = false;
   h->fused = true;
   return CHASE_OK;
@@ -1345,7 +1375,44 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
       const int rem = g.N % BNf;
       const bool split_w = !no_narrow && rem != 0 && (rem + BNn - 1) / BNn * BNn < BNf;
       const int Nmain = split_w ? g.N - rem : g.N;
-      ProfScope ps(h, odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN, split_w && Nmain > 0 ? 2 : 1);
+      const int cat = odd ? CAT_HEMM_ODD : CAT_HEMM_EVEN;
+      ProfScope ps(h, cat, 0);
+      // wave tail (fused_tail.cuh): when the step's tiles leave the persistent grid's last round
+      // partly idle, the fused kernel runs the first T_main tiles and the last T_tail tiles are
+      // split over K and reduced through the tail slots (slot pair per step parity, alternating)
+      static const bool no_tail = getenv("CHASE_FUSED_NO_TAIL") != nullptr;
+      const int G = h->sm_budget > 0 ? std::min(h->sm_budget, h->num_sms) : h->num_sms;
+      // the plan must be identical on every member (they process the same tile sets): K = the
+      // member's local rows differs by up to a block across members, so plan with the largest
+      const int Kplan = (int)(odd ? FL.ldc : FL.ldb);
+      const int KTf = (Kplan + (cplx ? ZG_BK : DG_BKT) - 1) / (cplx ? ZG_BK : DG_BKT);
+      const int tslot = (odd ? 0 : 2) + (int)(h->fused_tail_k[odd ? 0 : 1]++ & 1u);
+      FusedTailArgs tbase{};
+      tbase.m = m;
+      tbase.me = f.me;
+      tbase.M = g.M;
+      tbase.ldo = g.ldo;
+      tbase.ldx = g.ldx;
+      tbase.alpha = g.alpha;
+      tbase.beta = g.beta;
+      tbase.c = g.c;
+      tbase.owner_beta = f.owner_beta;
+      tbase.band_lo = g.band_lo;
+      tbase.band_hi = g.band_hi;
+      tbase.band_shift = g.band_shift;
+      tbase.band_map = g.band_map;
+      tbase.err = h->d_err;
+      tbase.sub = (long long)FUSED_TAIL_TILES * 128 * 128 * 8 / es;   // elements per sub-slot
+      for (int i = 0; i < m; ++i) {
+        const int w = odd ? i * h->q + h->mycol : h->myrow * h->q + i;
+        char* base = h->fz_base[w];
+        tbase.tp[i] = base + FL.tailp + (size_t)tslot * std::max(h->p, h->q) * FUSED_TAIL_TILES * 128 * 128 * 8;
+        tbase.tflag[i] = reinterpret_cast<unsigned*>(base + FL.tflags) + (size_t)tslot * FUSED_MAX_MEMBERS;
+      }
+      FusedTailArgs tpend[2];
+      void* tout[2] = {nullptr, nullptr};
+      bool tnar[2] = {false, false};
+      int npend = 0, slot_used = 0;
       int tile_base = 0;
       for (int part = 0; part < (split_w ? 2 : 1); ++part) {
         GemmReq gp = g;
@@ -1364,12 +1431,85 @@ chase_status_t chase_filter(chase_handle_t h, const void* A_local, int64_t lda, 
         }
         if (gp.N <= 0) continue;
         const int T = ((gp.M + BMf - 1) / BMf) * ((gp.N + (nar ? BNn : BNf) - 1) / (nar ? BNn : BNf));
+        int tS = 1, tail = 0;
+        if (!no_tail && !f.plain && T >= G)
+          plan_tail(T, KTf, G, FUSED_TAIL_TILES - slot_used, &tS, &tail);
+        const int tmain = T - tail;
         fp.tile_base = tile_base;
-        fp.ep = ++h->fused_ep;
-        CUDA_TRY(cudaMemsetAsync(f.tile_ctr, 0, sizeof(unsigned long long), h->stream));
-        STATUS_TRY(launch_zgemm_fused(h, gp.conj, *gp.tA, *gp.tX, gp, fp, T, nar));
+        fp.tiles = tail > 0 ? tmain : 0;
+        if (tmain > 0) {
+          fp.ep = ++h->fused_ep;
+          CUDA_TRY(cudaMemsetAsync(f.tile_ctr, 0, sizeof(unsigned long long), h->stream));
+          STATUS_TRY(launch_zgemm_fused(h, gp.conj, *gp.tA, *gp.tX, gp, fp, tmain, nar));
+          h->launches[cat] += 1;
+          h->fused_delivered += (unsigned long long)tmain;
+        } else if (tail > 0) {
+          // no fused kernel to wait for the previous step's deliveries: the split-K tail reads them
+          fused_wait_kernel<<<1, 1, 0, h->stream>>>(f.done[f.me], h->fused_delivered, h->d_err);
+          CUDA_TRY(cudaGetLastError());
+          h->launches[cat] += 1;
+        }
         tile_base += T;
-        h->fused_delivered += (unsigned long long)T;
+        if (tail == 0) continue;
+        GemmReq t = gp;
+        t.narrow = nar ? 1 : 0;
+        t.tX_narrow = nullptr;
+        t.k_split = tS;
+        t.tail_tiles = tail;
+        t.tile_offset = tmain;
+        t.out = h->tailws;
+        t.ldo = BMf;
+        t.alpha = 1.0; t.beta = 0.0; t.c = 0.0; t.use_beta = 0;
+        t.band_lo = t.band_hi = 0; t.band_shift = 0; t.band_map = nullptr;
+        STATUS_TRY(run_gemm(h, t));
+        FusedTailArgs ta = tbase;
+        ta.S = tS;
+        ta.tail_tiles = tail;
+        ta.tile_offset = tmain;
+        ta.slot_off = slot_used;
+        ta.N = gp.N;
+        if (cplx && !nar)
+          fused_tail_publish_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M><<<tail, 256, 0, h->stream>>>(
+              reinterpret_cast<const double2*>(h->tailws), static_cast<const double2*>(gp.xin), ta);
+        else if (cplx)
+          fused_tail_publish_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M><<<tail, 256, 0, h->stream>>>(
+              reinterpret_cast<const double2*>(h->tailws), static_cast<const double2*>(gp.xin), ta);
+        else if (!nar)
+          fused_tail_publish_kernel<double, DG_BM, DG_BN, DG_GROUP_M><<<tail, 256, 0, h->stream>>>(
+              reinterpret_cast<const double*>(h->tailws), static_cast<const double*>(gp.xin), ta);
+        else
+          fused_tail_publish_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M><<<tail, 256, 0, h->stream>>>(
+              reinterpret_cast<const double*>(h->tailws), static_cast<const double*>(gp.xin), ta);
+        CUDA_TRY(cudaGetLastError());
+        h->launches[cat] += 2;                 // split-K copies + publish
+        tpend[npend] = ta;
+        tout[npend] = fp.out[f.me];
+        tnar[npend] = nar;
+        ++npend;
+        slot_used += tail;
+      }
+      if (npend > 0) {
+        tbase.ep = ++h->fused_ep;
+        fused_tail_sync_kernel<<<1, 1, 0, h->stream>>>(tbase);
+        CUDA_TRY(cudaGetLastError());
+        h->launches[cat] += 1 + npend;
+        for (int i = 0; i < npend; ++i) {
+          FusedTailArgs ta = tpend[i];
+          const int nt = ta.tail_tiles;
+          if (cplx && !tnar[i])
+            fused_tail_reduce_kernel<double2, ZG_BM, ZG_BN, ZG_GROUP_M><<<nt, 256, 0, h->stream>>>(
+                static_cast<double2*>(tout[i]), ta);
+          else if (cplx)
+            fused_tail_reduce_kernel<double2, ZG_BM, ZG_BN_NARROW, ZG_GROUP_M><<<nt, 256, 0, h->stream>>>(
+                static_cast<double2*>(tout[i]), ta);
+          else if (!tnar[i])
+            fused_tail_reduce_kernel<double, DG_BM, DG_BN, DG_GROUP_M><<<nt, 256, 0, h->stream>>>(
+                reinterpret_cast<double*>(tout[i]), ta);
+          else
+            fused_tail_reduce_kernel<double, DG_BM, DG_BN_NARROW, DG_GROUP_M><<<nt, 256, 0, h->stream>>>(
+                reinterpret_cast<double*>(tout[i]), ta);
+          CUDA_TRY(cudaGetLastError());
+        }
       }
       continue;
     }

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (g.N + BN_ - 1) / BN_, m_tiles = (g.M + DG_BM - 1) / DG_BM;
-  const int T = n_tiles * m_tiles;
+  const int T = f.tiles > 0 ? f.tiles : n_tiles * m_tiles;
   const int KT = (g.K + DG_BKT - 1) / DG_BKT;
   constexpr int RING = ST_ + 4;                  // see zgemm_fused.cuh (grab 2 ahead)
   __shared__ int s_tile[RING];
@@ -181,10 +181,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         if (ok[i])
           for (int dst = 0; dst < f.m; ++dst) outs[dst][io[i]] = sum[i];
     }
-    __threadfence_system();
+    // the CTA's stores happen before thread 0's system fence (bar.sync), which publishes them
+    // all before the counters move (one fence per CTA, not one per thread)
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+      __threadfence_system();
       for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+    }
   };
 
   // Owned tiles wait in a small queue and are reduced as soon as all m partials are in, checked
@@ -276,8 +279,7 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
             slot[(long long)row + (long long)(f.col_base + col) * f.ldP] = v * g.alpha;
           }
         }
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();                           // then one system release by thread 0
     if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)(f.tile_base + t) * f.m + f.me, f.ep);
     if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
       s_q[s_qt % FUSED_QCAP] = t;

@@ -56,6 +56,8 @@ struct FusedArgs {
   int col_base;                              // staging-slot column offset of this launch's tiles
                                              //   (a step split into a wide-tile launch and a
                                              //   narrow-tile remainder launch keeps the two apart)
+  int tiles;                                 // > 0: only the first `tiles` tiles of the raster (the
+                                             //   rest is a split-K tail, fused_tail.cuh)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = (g.N + BN_ - 1) / BN_, m_tiles = (g.M + ZG_BM - 1) / ZG_BM;
-  const int T = n_tiles * m_tiles;
+  const int T = f.tiles > 0 ? f.tiles : n_tiles * m_tiles;
   const int KT = (g.K + ZG_BK - 1) / ZG_BK;
   // dynamic tile scheduler: tiles come from a global counter into a small smem ring (tile -1 =
   // no more tiles).  k-tile issue index q maps to (seq, kt) = (q / KT, q % KT); the refill duty
@@ -276,10 +278,13 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
         if (ok[i])
           for (int dst = 0; dst < f.m; ++dst) f.out[dst][io[i]] = sum[i];
     }
-    __threadfence_system();
+    // the CTA's stores happen before thread 0's system fence (bar.sync), which publishes them
+    // all before the counters move (one fence per CTA, not one per thread)
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
+      __threadfence_system();
       for (int dst = 0; dst < f.m; ++dst) atomicAdd_system(f.done[dst], 1ull);
+    }
   };
 
   // Owned tiles wait in a small queue and are reduced as soon as all m partials are in, checked
@@ -384,8 +389,7 @@ __global__ void __launch_bounds__(ZG_THREADS, 1)
             slot[(long long)row + (long long)(f.col_base + col) * f.ldP] = make_double2(vr * g.alpha, vi * g.alpha);
           }
         }
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();                           // then one system release by thread 0
     if (threadIdx.x == 0) st_release_sys_u32(f.flags[owner] + (long long)(f.tile_base + t) * f.m + f.me, f.ep);
     if (threadIdx.x == 0 && owner == f.me) {       // reduce it later, without blocking now
       s_q[s_qt % FUSED_QCAP] = t;

@@ -138,6 +138,61 @@ def test_virtual_grid_fused_matches_oracle(complex_, grid, nb):
 
 
 @pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("grid,nb,N,budget", [((2, 1), 0, 301, 2), ((2, 2), 0, 301, 2), ((1, 4), 0, 301, 2),
+                                              ((2, 2), 16, 301, 2), ((2, 1), 0, 700, 4), ((2, 4), 9, 700, 2)])
+def test_virtual_grid_fused_tail_matches_oracle(complex_, grid, nb, N, budget):
+    """A small persistent grid (sm_budget CTAs) leaves a partial last round on most steps, so the
+    fused step runs T_main tiles in the fused kernel and the rest as split-K copies reduced
+    through the tail slots (fused_tail.cuh): result = oracle, replicas bitwise identical, bitwise
+    repeatable (run_virtual runs twice)."""
+    p, q = grid
+    degs = sorted(RAGGED * 3)
+    A, V0, b = problem(N, degs, complex_, 79)
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    outs, rows, _ = run_virtual(A, V0, degs, b, p, q, nb, complex_, budget=budget)
+    for r, (V, ri) in enumerate(zip(outs, rows)):
+        assert colwise_rel(V, ref[ri]) <= TOL, f"rank {r}"
+    for i in range(p):
+        for j in range(1, q):
+            assert np.array_equal(outs[i * q], outs[i * q + j])
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+@pytest.mark.parametrize("grid,budget", [((2, 1), 5), ((2, 2), 3), ((1, 2), 5)])
+def test_virtual_grid_fused_tail_wide_and_narrow(complex_, grid, budget):
+    """Ragged width: one wide-tile and one narrow-tile launch per step (k = 84 complex: 64 + 20
+    columns; k = 140 real: 128 + 12), each with a split-K tail on 16 m-tiles over a 3- or 5-CTA
+    grid -- both launches' tails share the step's tail slot (wide and narrow tiles, one place
+    each)."""
+    p, q = grid
+    N = 2000
+    degs = [6] * (84 if complex_ else 140)
+    A, V0, b = problem(N, degs, complex_, 83)
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    outs, rows, _ = run_virtual(A, V0, degs, b, p, q, 0, complex_, budget=budget)
+    for r, (V, ri) in enumerate(zip(outs, rows)):
+        assert colwise_rel(V, ref[ri]) <= TOL, f"rank {r}"
+
+
+@pytest.mark.parametrize("complex_", [True, False])
+def test_fused_self_mode_tail_matches_oracle(complex_):
+    """1x1 fused self mode with a 3-CTA persistent grid: the tail path with m = 1."""
+    import torch
+    N, degs = 520, sorted(RAGGED * 3)
+    A, V0, b = problem(N, degs, complex_, 81)
+    ref, _ = oracle.chebyshev_filter(A, V0, degs, b.c, b.e, b.mu_1)
+    h = cb.Chase(cb.CHASE_C128 if complex_ else cb.CHASE_R64, N, len(degs))
+    region = torch.empty(cb.chase_fused_workspace_size(h.h), dtype=torch.uint8, device="cuda")
+    cb.chase_set_fused_workspace(h.h, region.data_ptr(), [region.data_ptr()])
+    cb.chase_set_fused_mode(h.h, 1, 3)
+    Vd = dev(V0)
+    h.filter(dev(A), Vd, degs, b.c, b.e, (b.mu_1, b.mu_ne, b.b_sup))
+    torch.cuda.synchronize()
+    assert colwise_rel(host(Vd), ref) <= TOL
+    h.close()
+
+
+@pytest.mark.parametrize("complex_", [True, False])
 @pytest.mark.parametrize("grid,nb", [((2, 2), 0), ((3, 2), 0), ((2, 3), 0), ((2, 2), 8), ((3, 2), 5)])
 @pytest.mark.parametrize("odd", [True, False])
 def test_filter_step_partials_match_oracle(complex_, grid, nb, odd):

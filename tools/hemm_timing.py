@@ -1,7 +1,9 @@
 """Time the filter HEMM kernels alone: one chase_filter call (after a warm-up call) with uniform
 degree D (or the C5 ramp 10..36) on an N x n problem; device time per odd / even step from the
 library's profile events, TFLOP/s from the algorithmic flops of those steps.
-Usage: python tools/hemm_timing.py N n [D|ramp] [real]"""
+Usage: python tools/hemm_timing.py N n [D|ramp] [real]
+FUSED_SELF=1: the 1x1 handle runs every step through the fused kernel (chase_set_fused_mode 1,
+optional FUSED_BUDGET CTAs) -- the fused protocol's own cost without NVLink."""
 import os
 import sys
 
@@ -23,6 +25,10 @@ A = gen.block(0, N, 0, N, device="cuda").T
 V = torch.from_numpy(np.ascontiguousarray(ci.gaussian_block(N, n, 1002, not real).T)).cuda().T
 b = ci.bounds_from_spectrum(lam, n)
 h = cb.Chase(cb.CHASE_R64 if real else cb.CHASE_C128, N, n)
+if os.environ.get("FUSED_SELF"):
+    region = torch.empty(cb.chase_fused_workspace_size(h.h), dtype=torch.uint8, device="cuda")
+    cb.chase_set_fused_workspace(h.h, region.data_ptr(), [region.data_ptr()])
+    cb.chase_set_fused_mode(h.h, 1, int(os.environ.get("FUSED_BUDGET", "0")))
 h.filter(A, V, degs, b.c, b.e, (b.mu_1, b.mu_ne, b.b_sup))
 torch.cuda.synchronize()
 cb.chase_profile_enable(h.h, True)
