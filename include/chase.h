@@ -189,7 +189,10 @@ chase_status_t chase_set_workspace(chase_handle_t h, void* dptr, size_t bytes);
  * ONE persistent kernel (zgemm_fused.cuh / dgemm_fused.cuh): the tensor-core HEMM publishes each partial output tile into its own
  * region, the tile's owner (tile mod m) sums the m partial tiles in fixed member order over
  * NVLink and stores the result into every member's region (P:149's AllReduce, done tile by tile
- * inside the GEMM, deterministic and replica-identical).  Without it, steps call ncclAllReduce.
+ * inside the GEMM, deterministic and replica-identical).  When the step's tiles leave the
+ * persistent grid's last round partly idle, its last tiles run instead as split-K copies whose
+ * partials every member pushes to every member and sums locally in the same fixed order
+ * (fused_tail.cuh; same bits on every member).  Without it, steps call ncclAllReduce.
  *
  * chase_fused_workspace_size: bytes of the symmetric region (identical on every rank).
  * chase_set_fused_workspace: local = this rank's region (device, 256-byte aligned, >= size);
