@@ -158,28 +158,47 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     tile_origin(t, m0, n0);
     double* const* outs = reinterpret_cast<double* const*>(f.out);
     const double* __restrict__ mine = reinterpret_cast<const double*>(f.P[f.me]);
-    constexpr int PER = DG_BM * BN_ / DG_THREADS;     // 64 elements per thread
-    constexpr int BATCH = 8;
+    // row pairs as double2 (ldP, ldo and slot are even, every column 16-byte aligned; the pair
+    // partner of an odd M's last row is padding, loaded and never stored): 64 BN_ pairs per tile,
+    // up to 16 per thread per batch, all their loads in flight together
+    constexpr int HM = DG_BM / 2;
+    constexpr int PER2 = HM * BN_ / DG_THREADS;       // 32 (BN 128) or 8 (BN 32)
+    constexpr int BATCH2 = PER2 < 16 ? PER2 : 16;
 #pragma unroll 1
-    for (int b0 = 0; b0 < PER; b0 += BATCH) {
-      double sum[BATCH];
-      long long io[BATCH];
-      bool ok[BATCH];
+    for (int b0 = 0; b0 < PER2; b0 += BATCH2) {
+      double2 sum[BATCH2];
 #pragma unroll
-      for (int i = 0; i < BATCH; ++i) {
+      for (int i = 0; i < BATCH2; ++i) {
         const int e = threadIdx.x + (b0 + i) * DG_THREADS;
-        const int row = m0 + (e % DG_BM), col = n0 + (e / DG_BM);
-        ok[i] = row < g.M && col < g.N;
-        const long long ip = (long long)row + (long long)(f.col_base + col) * f.ldP;
-        io[i] = (long long)row + (long long)col * g.ldo;
-        sum[i] = ok[i] ? mine[ip] : 0.0;
-        for (int src = 1; src < f.m; ++src) sum[i] += ok[i] ? mine[(long long)src * f.slot + ip] : 0.0;
-        if (f.owner_beta && ok[i]) sum[i] += g.beta * outs[f.me][io[i]];
+        const int row = m0 + 2 * (e % HM), col = n0 + e / HM;
+        sum[i] = make_double2(0.0, 0.0);
+        if (row < g.M && col < g.N) {
+          const long long ip = (long long)row + (long long)(f.col_base + col) * f.ldP;
+          sum[i] = *reinterpret_cast<const double2*>(mine + ip);
+          for (int src = 1; src < f.m; ++src) {
+            const double2 v = *reinterpret_cast<const double2*>(mine + (long long)src * f.slot + ip);
+            sum[i].x += v.x;
+            sum[i].y += v.y;
+          }
+          if (f.owner_beta) {
+            const double2 old = *reinterpret_cast<const double2*>(outs[f.me] + (long long)row + (long long)col * g.ldo);
+            sum[i].x += g.beta * old.x;
+            sum[i].y += g.beta * old.y;
+          }
+        }
       }
 #pragma unroll
-      for (int i = 0; i < BATCH; ++i)
-        if (ok[i])
-          for (int dst = 0; dst < f.m; ++dst) outs[dst][io[i]] = sum[i];
+      for (int i = 0; i < BATCH2; ++i) {
+        const int e = threadIdx.x + (b0 + i) * DG_THREADS;
+        const int row = m0 + 2 * (e % HM), col = n0 + e / HM;
+        if (row >= g.M || col >= g.N) continue;
+        const long long io = (long long)row + (long long)col * g.ldo;
+        if (row + 1 < g.M) {
+          for (int dst = 0; dst < f.m; ++dst) *reinterpret_cast<double2*>(outs[dst] + io) = sum[i];
+        } else {
+          for (int dst = 0; dst < f.m; ++dst) outs[dst][io] = sum[i].x;
+        }
+      }
     }
     // the CTA's stores happen before thread 0's system fence (bar.sync), which publishes them
     // all before the counters move (one fence per CTA, not one per thread)
