@@ -123,11 +123,11 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   struct Frag {
     double a[DG_MT][2], b[NT_];
   };
-  auto load = [&](Frag& fr, int gs, int kt, int sub) {
+  auto load = [&](Frag& fr, int st, int kt, int sub) {    // st: smem stage
     const int u = sub >> 2, hsub = sub & 3;
     const int k = dg_kperm(tq, hsub);
-    const uint8_t* sa = smem + (gs % ST_) * SB_ + u * SLA;
-    const uint8_t* sx = smem + (gs % ST_) * SB_ + AB_ + u * SLX;
+    const uint8_t* sa = smem + st * SB_ + u * SLA;
+    const uint8_t* sx = smem + st * SB_ + AB_ + u * SLX;
 #pragma unroll
     for (int mt = 0; mt < DG_MT; ++mt)
 #pragma unroll
@@ -312,23 +312,27 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
   int tile = s_tile[0];
   if (tile < 0) return;
   load(cur, 0, 0, 0);
-  int seq = 0, kt = 0, gs = 0;
+  // stage and phase of issue index gs kept incrementally (ST_ = 3 for the wide tile: a division
+  // per k-tile otherwise sits in front of every k-tile's first MMAs)
+  int seq = 0, kt = 0, gs = 0, stg = 0, ph = 0;
   for (;;) {
-    const int s = gs % ST_;
+    const int s = stg;
+    const int stn = stg + 1 == ST_ ? 0 : stg + 1;         // stage / phase of gs + 1
+    const int phn = stg + 1 == ST_ ? ph ^ 1 : ph;
     int next_tile = tile;
 #pragma unroll
     for (int sub = 0; sub < SUBS; ++sub) {
       if (sub + 1 < SUBS) {
-        load(nxt, gs, kt, sub + 1);
+        load(nxt, s, kt, sub + 1);
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        mbar_wait_dbg(&full[(gs + 1) % ST_], ((gs + 1) / ST_) & 1, 2, gs);
+        mbar_wait_dbg(&full[stn], phn, 2, gs);
         if (kt + 1 < KT) {
-          load(nxt, gs + 1, kt + 1, 0);
+          load(nxt, stn, kt + 1, 0);
         } else {
           next_tile = s_tile[(seq + 1) % RING];
-          if (next_tile >= 0) load(nxt, gs + 1, 0, 0);
+          if (next_tile >= 0) load(nxt, stn, 0, 0);
         }
       }
 #pragma unroll
@@ -338,11 +342,13 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       cur = nxt;
     }
     if (lane == 0 && warp == (gs & (DG_CONSUMERS - 1)) && gs >= 1) {
-      const int sp = (gs - 1) % ST_;
-      mbar_wait_dbg(&empty[sp], ((gs - 1) / ST_) & 1, 3, gs);
+      const int sp = stg == 0 ? ST_ - 1 : stg - 1;           // stage / phase of gs - 1
+      mbar_wait_dbg(&empty[sp], stg == 0 ? ph ^ 1 : ph, 3, gs);
       issue(gs - 1 + ST_, sp);
     }
     ++gs;
+    stg = stn;
+    ph = phn;
     if (++kt == KT) {
       epilogue(tile);
       zero_acc();
